@@ -1,0 +1,470 @@
+"""bench.py -- HDC / M-HDC SpMV on B200 (BASELINE.json metric: SpMV GFLOP/s at 2*nnz
+and HBM GB/s as a fraction of the roofline, at 1/2/4/8 GPUs).
+
+Default workload (every N): BASELINE config 4 -- the 7-point Dirichlet Laplacian
+on a 1024x1024x512 grid (n = 536,870,912, nnz = 3,753,902,080), M-HDC with
+bl = 4096, theta = 0.6, rows sharded in contiguous z-slabs over the N ranks,
+1,048,576-row x halo exchanged per SpMV, power iteration x <- y/||y|| from x
+uniform[-1,1] (seed 5).  One step = one power-iteration step = one SpMV over
+the whole matrix (+ its fused norm and halo exchange).  Total work is fixed as
+N grows -> "scaling": "strong".  The matrix (38.6 GB of algorithmic traffic per
+step) is far larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c1|c2|c3] [--format mhdc|hdc] [--bl B]
+
+Other workloads (c1..c3, single SpMV steps) are for DESIGN.md / profiling.
+--impl reference times the reference's own CPU spmv_mhdc (oracle/_ref, the
+unmodified library built from /root/reference) on a bounded sample of the
+same workload with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+GRID4 = (1024, 1024, 512)
+METRIC = "SpMV GFLOP/s (2*nnz)"
+UNIT = "GFLOP/s"
+THETA = 0.6
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def b_min(dia_slots, n_seg, n_blocks, nnz_rest, n_rows, halo_rows=0):
+    """Algorithmic bytes of one SpMV (model.cpp:62-72 with v_x = 1):
+    8 dia_slots + 4 n_seg + 4 (n_b+1) + [12 nnz_rest + 4 (n+1)] + 8 n (x) + 8 n (y) + 8 halo."""
+    b = 8 * dia_slots + 4 * n_seg + 4 * (n_blocks + 1) + 16 * n_rows + 8 * halo_rows
+    if nnz_rest > 0:
+        b += 12 * nnz_rest + 4 * (n_rows + 1)
+    return b
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(key):
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(key)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (bounded sample of the workload)
+
+def cpu_sample(workload):
+    """A bounded sample of the workload, as a standalone CSR the reference can take."""
+    from paper_2105_04937_b200 import synth
+    if workload == "c4":
+        nx, ny, nz = 1024, 1024, 16  # 16 z-planes of config 4: 16.7M rows, same stencil
+        return synth.laplacian7(nx, ny, nz), 4096, f"config-4 z-slab sample {nx}x{ny}x{nz} (16 of 512 planes)"
+    if workload == "c1":
+        return synth.laplacian7(256, 256, 256), 4096, "config 1 (256^3) in full"
+    if workload == "c2":
+        return synth.stencil27(96, seed=2), 4096, "config-2 sample: 27-point 96^3 (1/8 of the rows)"
+    return synth.quasi_diag(1 << 22, seed=4), 8192, "config-3 sample: n = 2^22 (1/4 of the rows)"
+
+
+def run_cpu_reference(workload, fmt, steps, warmup):
+    """Times the reference's CPU kernel with all host threads.  Returns a dict."""
+    (rp, col, val), bl, sample = cpu_sample(workload)
+    x = np.random.default_rng(5).uniform(-1, 1, len(rp) - 1)
+    nnz = int(rp[-1])
+    try:
+        from oracle.oracle import Ref
+        R = Ref()
+        kind = "reference"
+        h = R.hdc_handle(rp, col, val, THETA) if fmt == "hdc" else R.mhdc_handle(rp, col, val, THETA, bl)
+        cores = R.max_threads()
+
+        y = np.zeros_like(x)
+
+        def call():
+            R.spmv(fmt, h, x, out=y)
+    except Exception:  # reference library not built: the C port of it
+        from oracle.oracle import Port
+        P = Port()
+        kind = "port"
+        m = P.to_hdc(rp, col, val, THETA) if fmt == "hdc" else P.to_mhdc(rp, col, val, THETA, bl)
+        cores = P.max_threads()
+
+        y = np.zeros_like(x)
+
+        def call():
+            P.spmv_mhdc(m, x, 0, out=y)
+    for _ in range(warmup):
+        call()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    return {"value": 2.0 * nnz / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{sample}, {fmt} theta={THETA} bl={bl}, nnz={nnz}, {steps} timed calls "
+                      f"(mean {t * 1e3:.2f} ms) after {warmup} warm-up",
+            "ms_per_call": t * 1e3, "best_ms": min(times) * 1e3}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def build_config4_slab(H, torch, plan, rank, bl):
+    nx, ny, nz = GRID4
+    plane = nx * ny
+    row0, rows = plan.row0[rank], plan.rows[rank]
+    z0, z1 = row0 // plane, (row0 + rows) // plane
+    nnz = H.gen_laplacian7_nnz(nx, ny, nz, z0, z1)
+    rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+    col = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    val = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    H.gen_laplacian7(nx, ny, nz, z0, z1, rp.data_ptr(), col.data_ptr(), val.data_ptr())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    m = H.build_mhdc_device(rows, plan.n, row0, nnz, rp.data_ptr(), col.data_ptr(), val.data_ptr(),
+                            THETA, bl, rp64=True, validate=False)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    del rp, col, val
+    torch.cuda.empty_cache()
+    return m, nnz, t_build
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2105_04937_b200 import hdcgpu as H
+    from paper_2105_04937_b200.dist import CudaSlab, SlabPlan, SlabPowerIteration
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    H.init(local)
+
+    nx, ny, nz = GRID4
+    n = nx * ny * nz
+    halo = nx * ny
+    bl = a.bl or 4096
+    plan = SlabPlan.make(n, bl, halo, world, unit=nx * ny)
+    m, nnz_local, t_build = build_config4_slab(H, torch, plan, rank, bl)
+    rows, row0 = plan.rows[rank], plan.row0[rank]
+    info = m.info
+
+    # x buffer with halos, x0 = uniform[-1,1] seed 5 over global rows
+    xbuf = torch.zeros(rows + 2 * halo, dtype=torch.float64, device="cuda")
+    g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
+    H.gen_uniform_pm1(5, 0, g0, g1 - g0, xbuf.data_ptr() + 8 * (g0 - (row0 - halo)))
+    compute = CudaSlab(m, halo)
+    it = SlabPowerIteration(plan, rank, compute, xbuf, comm=world > 1)
+
+    # per-launch kernel events for the roofline (same stream as the kernels)
+    kernel_events = []
+    orig_spmv = compute.spmv
+
+    def timed_spmv(*args):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        orig_spmv(*args)
+        e.record()
+        kernel_events.append((s, e))
+
+    for _ in range(a.warmup):
+        it.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    compute.spmv = timed_spmv
+    launches0 = compute.launches
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(a.steps):
+            it.step()
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    compute.spmv = orig_spmv
+    launches = compute.launches - launches0
+    ms_local = start.elapsed_time(end) / a.steps
+    kern_ms_local = sum(s.elapsed_time(e) for s, e in kernel_events) / a.steps
+    norm2 = float(it.red[0].item())
+
+    # ---- e2e through the public host API: H2D x, SpMV, D2H y per step ----------------
+    e2e_steps = max(1, min(a.steps, 5))
+    x_host = torch.empty(g1 - g0, dtype=torch.float64).pin_memory()
+    x_host.copy_(xbuf[g0 - (row0 - halo):g1 - (row0 - halo)].cpu())
+    y_host = torch.empty(rows, dtype=torch.float64).pin_memory()
+    if world == 1:
+        def e2e_call():
+            H.check(H.lib().hdcg_spmv_host(m.handle, x_host.data_ptr(), y_host.data_ptr()))
+        h2d, d2h = 8 * n, 8 * n
+    else:
+        xd = torch.zeros(rows + 2 * halo, dtype=torch.float64, device="cuda")
+        yd = torch.empty(rows, dtype=torch.float64, device="cuda")
+
+        def e2e_call():
+            xd[g0 - (row0 - halo):g1 - (row0 - halo)].copy_(x_host, non_blocking=True)
+            H.spmv_slab(m, xd.data_ptr() + 8 * halo, yd.data_ptr(), 0, m.n_blocks, 0, 0,
+                        torch.cuda.current_stream().cuda_stream)
+            y_host.copy_(yd, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        h2d, d2h = 8 * (g1 - g0), 8 * rows
+    e2e_call()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_call()
+    e2e_s_local = (time.perf_counter() - t0) / e2e_steps
+
+    # ---- max over ranks -----------------------------------------------------------
+    vec = torch.tensor([ms_local, kern_ms_local, e2e_s_local], dtype=torch.float64, device="cuda")
+    nnz_t = torch.tensor([nnz_local], dtype=torch.int64, device="cuda")
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nnz_t, op=dist.ReduceOp.SUM)
+    ms, kern_ms, e2e_s = vec.tolist()
+    nnz_total = int(nnz_t.item())
+
+    result = None
+    if rank == 0:
+        flops = 2.0 * nnz_total
+        value = flops / (ms * 1e-3) / 1e9
+        bytes_local = b_min(info.dia_slots, info.n_seg, info.n_blocks, info.nnz_rest, rows,
+                            halo_rows=(0 if world == 1 else 2 * halo))
+        peak, peak_kind = load_peaks()
+        achieved = bytes_local / (kern_ms_local * 1e-3) / 1e9
+        traffic = load_traffic(f"c4_bl{bl}_n{world}")
+        result = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE config 4 generated on device; x uniform[-1,1] seed 5)",
+            "config": {"workload": "config4: 7-pt Laplacian 1024x1024x512, M-HDC bl=%d theta=0.6, "
+                                   "power iteration x<-y/||y||" % bl,
+                       "n": n, "nnz": nnz_total, "bl": bl, "theta": THETA,
+                       "parallelism": f"row-slab x{world} (z-slabs), halo {halo} rows via NCCL P2P",
+                       "l2": "inputs larger than L2 (38.6 GB/step >> 126 MB); no flush needed",
+                       "n_seg_rank0": info.n_seg, "nnz_rest_rank0": info.nnz_rest,
+                       "convert_s_rank0": round(t_build, 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "algorithmic_bytes_per_launch": bytes_local,
+                         "kernel_ms": round(kern_ms_local, 4), "peak_source": f"{peak_kind} hbm_gbs",
+                         "kernel": "hdcg::spmv_kernel<2,true,true>"},
+            "e2e": {"value": round(flops / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
+                    "api": "hdcg_spmv_host (pinned host x/y)" if world == 1 else "per-rank H2D+spmv_slab+D2H"},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "norm2_last": norm2,
+        }
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            result["cpu_baseline"] = run_cpu_reference("c4", "mhdc", steps=10, warmup=2)
+        except Exception as e:  # never lose the GPU line over the CPU baseline
+            result["cpu_baseline"] = {"value": None, "error": repr(e)[:200]}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    m.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_ours_single(a):
+    """c1 / c2 / c3: one device-resident matrix, one SpMV per step (N = 1)."""
+    import torch
+    from paper_2105_04937_b200 import hdcgpu as H
+    from paper_2105_04937_b200 import synth
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    H.init(local)
+    if a.workload == "c1":
+        (rp, col, val), bl, seed, label = synth.laplacian7(256, 256, 256), 4096, 1, "config1: 7-pt 256^3"
+    elif a.workload == "c2":
+        (rp, col, val), bl, seed, label = synth.stencil27(192, 2), 4096, 3, "config2: 27-pt 192^3"
+    else:
+        (rp, col, val), bl, seed, label = synth.quasi_diag(1 << 24, 4), 8192, 4, "config3: quasi-diagonal 2^24"
+    bl = a.bl or bl
+    n = len(rp) - 1
+    A = H.CsrMatrix(n, val, col, rp.astype(np.int32))
+    t0 = time.perf_counter()
+    m = H.to_hdc(A, THETA, validate=False) if a.format == "hdc" else H.to_mhdc(A, THETA, bl, validate=False)
+    t_build = time.perf_counter() - t0
+    info = m.info
+    x = torch.from_numpy(synth.x_vector(n, seed)).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(a.warmup):
+        H.spmv_device(m, x.data_ptr(), y.data_ptr(), st)
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clocks:
+        for _ in range(a.steps):
+            flush.fill_(1.0)  # 256 MB write: evicts L2 between timed launches
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            H.spmv_device(m, x.data_ptr(), y.data_ptr(), st)
+            e.record()
+            times.append((s, e))
+        torch.cuda.synchronize()
+    ms = statistics.mean(s.elapsed_time(e) for s, e in times)
+    peak, peak_kind = load_peaks()
+    bts = b_min(info.dia_slots, info.n_seg, info.n_blocks, info.nnz_rest, n)
+    nnz = int(rp[-1])
+    xh = torch.from_numpy(synth.x_vector(n, seed)).pin_memory()
+    yh = torch.empty(n, dtype=torch.float64).pin_memory()
+    H.check(H.lib().hdcg_spmv_host(m.handle, xh.data_ptr(), yh.data_ptr()))
+    t0 = time.perf_counter()
+    for _ in range(5):
+        H.check(H.lib().hdcg_spmv_host(m.handle, xh.data_ptr(), yh.data_ptr()))
+    e2e = (time.perf_counter() - t0) / 5
+    out = {
+        "metric": METRIC, "value": round(2 * nnz / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "n_gpus": 1,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{label}, {a.format} theta=0.6" + ("" if a.format == "hdc" else f" bl={bl}"),
+                   "n": n, "nnz": nnz, "n_seg": info.n_seg, "nnz_rest": info.nnz_rest,
+                   "dia_slots": info.dia_slots, "convert_s": round(t_build, 3),
+                   "l2": "256 MB L2 flush before every timed launch"},
+        "roofline": {"bound": "hbm", "achieved": round(bts / (ms * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(bts / (ms * 1e-3) / 1e9 / peak, 4),
+                     "traffic": load_traffic(f"{a.workload}_{a.format}_bl{bl}"),
+                     "algorithmic_bytes_per_launch": bts, "peak_source": f"{peak_kind} hbm_gbs"},
+        "e2e": {"value": round(2 * nnz / e2e / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": a.steps,
+        "clocks": clocks.summary(),
+    }
+    if not a.no_cpu_baseline:
+        out["cpu_baseline"] = run_cpu_reference(a.workload, a.format, steps=10, warmup=2)
+    print(json.dumps(out), flush=True)
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    r = run_cpu_reference(a.workload, a.format, steps=a.steps, warmup=a.warmup)
+    out = {
+        "metric": METRIC, "value": round(r["value"], 3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(r["ms_per_call"], 3), "higher_is_better": True,
+        "scaling": "strong" if a.workload == "c4" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{a.workload} sample on the host CPU: {r['sample']}"},
+        "cpu_baseline": r,
+        "e2e": {"value": round(r["value"], 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c4", "c1", "c2", "c3"], default="c4")
+    ap.add_argument("--format", choices=["mhdc", "hdc"], default="mhdc")
+    ap.add_argument("--bl", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    a = ap.parse_args(argv)
+    if a.impl == "reference":
+        return run_reference(a)
+    if a.workload == "c4":
+        return run_ours(a)
+    return run_ours_single(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,135 @@
+// Internal declarations shared by the CUDA translation units of libhdcgpu.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "hdcgpu.h"
+
+namespace hdcg {
+
+// ---- errors ---------------------------------------------------------------
+// Internal code throws Error; the C-ABI layer (capi.cu) converts it into an
+// hdcg_status + message.  Nothing ever falls back to the CPU.
+struct Error : std::runtime_error {
+    hdcg_status status;
+    Error(hdcg_status s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] inline void fail(hdcg_status s, const std::string& msg) { throw Error(s, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation)
+        fail(HDCG_ERR_OUT_OF_MEMORY, std::string(what) + ": " + cudaGetErrorString(e));
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver ||
+        e == cudaErrorNoKernelImageForDevice)
+        fail(HDCG_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(HDCG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define HDCG_CUDA(call) ::hdcg::cuda_check((call), #call)
+#define HDCG_LAUNCH_CHECK(name) ::hdcg::cuda_check(cudaGetLastError(), name)
+
+// ---- the device-resident matrix -------------------------------------------
+// One storage layout serves M-HDC, HDC (bl = n, one block, lanes) and CSR
+// (no diagonal part):
+//   dia_ptr  int32[n_blocks+1]  exclusive prefix of per-block segment counts
+//   dia_off  int32[n_seg]       ascending within a block
+//   seg      f64[n_seg*bl]      segment k at [k*bl, (k+1)*bl), slot = i - ib*bl
+//   rest_rp  int32[n_rows+1]    remainder CSR (rows local, columns global)
+//   rest_col int32[nnz_rest]
+//   rest_val f64[nnz_rest]
+struct Matrix {
+    hdcg_kind kind = HDCG_KIND_MHDC;
+    int device = 0;
+    int64_t n_rows = 0, n_cols = 0, row0 = 0, bl = 1, n_blocks = 0;
+    int64_t n_seg = 0, nnz_rest = 0, nnz_input = 0, dia_slots = 0;
+    int32_t* dia_ptr = nullptr;
+    int32_t* dia_off = nullptr;
+    double* seg = nullptr;
+    int32_t* rest_rp = nullptr;
+    int32_t* rest_col = nullptr;
+    double* rest_val = nullptr;
+    // lazily allocated staging for hdcg_spmv_host
+    double* dx = nullptr;
+    double* dy = nullptr;
+    cudaStream_t host_stream = nullptr;
+    cudaEvent_t host_events[2] = {nullptr, nullptr};
+    int64_t device_bytes = 0;
+};
+
+void matrix_release(Matrix* m);
+
+// ---- SpMV tiling -----------------------------------------------------------
+// A tile is the row range one CTA owns.  Tiles never straddle a block: when
+// bl >= tile_rows a block holds ceil(len/tile_rows) tiles; otherwise a tile
+// holds G = tile_rows / bl whole blocks.
+struct Tiling {
+    int rows_per_thread;   // 2 (double2 segment loads) or 1 (odd bl)
+    int64_t tile_rows;     // threads * rows_per_thread
+    int64_t tiles_per_block;  // > 0 when bl >= tile_rows
+    int64_t blocks_per_tile;  // > 0 when bl <  tile_rows
+    int64_t n_tiles;
+};
+Tiling tiling_of(const Matrix& m);
+
+void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin,
+                 int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st);
+void tree_sum_launch(const double* vals, int64_t count, double* out, cudaStream_t st);
+
+// ---- converters (convert.cu) ------------------------------------------------
+struct CsrInput {
+    int64_t n_rows, n_cols, row0, nnz;
+    const void* row_ptr;  // device
+    bool rp64;
+    const int32_t* col;   // device
+    const double* val;    // device (may be null for census-only)
+};
+void validate_csr(const CsrInput& in, cudaStream_t st);
+void build_mhdc(const CsrInput& in, double theta, int64_t bl, Matrix* out, cudaStream_t st);
+void build_hdc(const CsrInput& in, double theta, Matrix* out, cudaStream_t st);
+void build_csr(const CsrInput& in, Matrix* out, cudaStream_t st);
+// census: returns the number of (block, offset) entries; fills host arrays when non-null
+int64_t census(const CsrInput& in, int64_t bl, int64_t* block_ptr_host, int32_t* offsets_host,
+               int64_t* counts_host, cudaStream_t st);
+void rates(const Matrix& m, double* alpha, double* beta, int64_t* slots, cudaStream_t st);
+// CUB exclusive scan of int64 (defined in convert.cu so only one TU includes CUB)
+cudaError_t cub_exclusive_sum_i64(void* tmp, size_t& bytes, const int64_t* in, int64_t* out,
+                                  int64_t count, cudaStream_t st);
+
+// ---- small device helpers ----------------------------------------------------
+template <class T>
+T* dev_alloc(int64_t count, cudaStream_t st) {
+    if (count <= 0) return nullptr;
+    void* p = nullptr;
+    HDCG_CUDA(cudaMallocAsync(&p, sizeof(T) * (size_t)count, st));
+    return static_cast<T*>(p);
+}
+template <class T>
+void dev_free(T* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t n_blocks_of(int64_t n, int64_t bl) { return n == 0 ? 0 : ceil_div(n, bl); }
+
+inline int grid_cap(int64_t want) {
+    const int64_t cap = 148LL * 64;  // enough CTAs for any grid-stride kernel
+    return (int)(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+// splitmix64 counter RNG (synth.py)
+__host__ __device__ inline uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ inline uint64_t stream_key(uint64_t seed, uint64_t stream) {
+    return splitmix64(seed * 0x9E3779B97F4A7C15ULL + stream * 0xD1B54A32D192ED03ULL);
+}
+
+}  // namespace hdcg

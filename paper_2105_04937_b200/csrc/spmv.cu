@@ -1,0 +1,320 @@
+// spmv.cu -- the HDC / M-HDC SpMV kernel family for sm_100a.
+//
+// Replaces hdc::spmv_mhdc (proj/src/kernels.cpp:173-206) and, because their
+// per-row accumulation order is the same, spmv_hdc / spmv_bhdc
+// (kernels.cpp:107-171), spmv_dia / spmv_bdia (:56-105) and spmv_csr (:39-54).
+//
+// Per row i the reference computes
+//     s = +0.0;  for k in rest_row(i) (stored order): s += val[k] * x[col[k]]
+//     for each segment / lane k of i's block, ascending: if 0 <= i+off_k < n: s += seg_k[i] * x[i+off_k]
+// with separately rounded multiply and add (the x86-64 oracle has no FMA).
+// This kernel performs exactly those floating-point operations in exactly
+// that order (__dmul_rn / __dadd_rn), so y is bitwise equal to the reference.
+//
+// Layout / bandwidth design (memory-bound fp64 streaming reduction, no tensor
+// cores):
+//   * one CTA owns a tile of 256*R rows inside one row block (or G whole
+//     blocks when bl < tile); thread t owns R consecutive rows;
+//   * segment values are streamed once with 128-bit evict-first loads
+//     (ld.global.cs.v2.f64) -- 8 B/slot, the dominant traffic;
+//   * the block's segment loop is unrolled by SEG_UNROLL with all loads issued
+//     before the dependent adds, so each thread keeps ~8 x 16 B in flight;
+//   * x is read through the L1/tex path: the near offsets (-1,0,+1 ...) of a
+//     tile share lines in L1, far offsets (+-nx, +-nx*ny) hit L2 because the
+//     wavefront of resident tiles re-reads them within ~2*nx*ny rows;
+//   * the CSR remainder of the tile is processed in chunks: the products
+//     val[k]*x[col[k]] are computed by all threads with coalesced loads into
+//     shared memory, then each thread sums its own rows sequentially in stored
+//     order (bitwise order preserved, no warp-tree reordering);
+//   * y is written once (streaming store); optional fused epilogue emits the
+//     tile's sum of y_i^2 (power iteration) in a fixed reduction order.
+#include "hdcg_internal.cuh"
+
+namespace hdcg {
+
+constexpr int SPMV_THREADS = 256;
+constexpr int REST_CHUNK = 1024;  // doubles of staged remainder products
+constexpr int SEG_UNROLL = 8;
+
+struct SpmvArgs {
+    const int32_t* dia_ptr;
+    const int32_t* dia_off;
+    const double* seg;
+    const int32_t* rest_rp;
+    const int32_t* rest_col;
+    const double* rest_val;
+    const double* x;  // x_local: x_local[j - row0] = x_j
+    double* y;
+    const double* x_scale;
+    double* tile_sumsq;
+    int64_t n_rows, n_cols, row0, bl;
+    int64_t tiles_per_block, blocks_per_tile, tile_rows;
+    int64_t tile_begin;
+    int has_rest;
+    int y_vec_ok;
+};
+
+template <int R, bool SCALE, bool NORM>
+__global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
+    __shared__ double prod[REST_CHUNK];
+    __shared__ double warp_sums[SPMV_THREADS / 32];
+
+    const int64_t tile = a.tile_begin + blockIdx.x;
+    int64_t lo, hi;
+    if (a.tiles_per_block > 0) {
+        const int64_t b = tile / a.tiles_per_block;
+        const int64_t t = tile - b * a.tiles_per_block;
+        const int64_t b0 = b * a.bl;
+        const int64_t bend = min(b0 + a.bl, a.n_rows);
+        lo = b0 + t * a.tile_rows;
+        hi = min(lo + a.tile_rows, bend);
+    } else {
+        lo = tile * a.blocks_per_tile * a.bl;
+        hi = min(lo + a.blocks_per_tile * a.bl, a.n_rows);
+    }
+    const int64_t i0 = lo + (int64_t)R * threadIdx.x;
+
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    double sc = 1.0;
+    if (SCALE) sc = *a.x_scale;
+
+    // ---- CSR remainder: products staged in smem, per-row sequential sums ----
+    if (a.has_rest && lo < hi) {
+        const int64_t e_lo = a.rest_rp[lo];
+        const int64_t e_hi = a.rest_rp[hi];
+        if (e_lo < e_hi) {
+            int64_t kb[R], ke[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int64_t i = i0 + r;
+                if (i < hi) {
+                    kb[r] = a.rest_rp[i];
+                    ke[r] = a.rest_rp[i + 1];
+                } else {
+                    kb[r] = ke[r] = 0;
+                }
+            }
+            for (int64_t c0 = e_lo; c0 < e_hi; c0 += REST_CHUNK) {
+                const int64_t c1 = min(c0 + (int64_t)REST_CHUNK, e_hi);
+                for (int64_t e = c0 + threadIdx.x; e < c1; e += SPMV_THREADS) {
+                    double xv = __ldg(a.x + ((int64_t)__ldcs(a.rest_col + e) - a.row0));
+                    if (SCALE) xv = __dmul_rn(xv, sc);
+                    prod[e - c0] = __dmul_rn(__ldcs(a.rest_val + e), xv);
+                }
+                __syncthreads();
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int64_t k0 = max(kb[r], c0), k1 = min(ke[r], c1);
+                    for (int64_t k = k0; k < k1; ++k) acc[r] = __dadd_rn(acc[r], prod[k - c0]);
+                }
+                __syncthreads();
+            }
+        }
+    }
+
+    // ---- diagonal segments of this row's block, stored order ----------------
+    if (i0 < hi) {
+        const int64_t b = i0 / a.bl;
+        const int64_t l = i0 - b * a.bl;
+        const int k0 = __ldg(a.dia_ptr + b);
+        const int k1 = __ldg(a.dia_ptr + b + 1);
+        const int64_t gi = a.row0 + i0;
+        const double* seg_base = a.seg + l;
+        for (int k = k0; k < k1; k += SEG_UNROLL) {
+            double v[SEG_UNROLL][R];
+            double xv[SEG_UNROLL][R];
+#pragma unroll
+            for (int u = 0; u < SEG_UNROLL; ++u) {
+                const int kk = k + u;
+#pragma unroll
+                for (int r = 0; r < R; ++r) { v[u][r] = 0.0; xv[u][r] = 0.0; }
+                if (kk < k1) {
+                    const int64_t o = __ldg(a.dia_off + kk);
+                    const double* sp = seg_base + (int64_t)kk * a.bl;
+                    if (R == 2) {
+                        const double2 t = __ldcs(reinterpret_cast<const double2*>(sp));
+                        v[u][0] = t.x;
+                        v[u][R - 1] = t.y;
+                    } else {
+                        v[u][0] = __ldcs(sp);
+                    }
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int64_t j = gi + r + o;
+                        const bool ok = (j >= 0) & (j < a.n_cols) & (i0 + r < hi);
+                        if (ok) xv[u][r] = __ldg(a.x + (i0 + r + o));
+                    }
+                }
+            }
+            // zero slots contribute +-0.0, an identity on an accumulator that
+            // can never be -0.0 (it starts at +0.0), so masked rows add nothing.
+#pragma unroll
+            for (int u = 0; u < SEG_UNROLL; ++u) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    double xx = xv[u][r];
+                    if (SCALE) xx = __dmul_rn(xx, sc);
+                    acc[r] = __dadd_rn(acc[r], __dmul_rn(v[u][r], xx));
+                }
+            }
+        }
+        if (R == 2 && a.y_vec_ok && i0 + 1 < hi) {
+            __stcs(reinterpret_cast<double2*>(a.y + i0), make_double2(acc[0], acc[R - 1]));
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (i0 + r < hi) __stcs(a.y + i0 + r, acc[r]);
+        }
+    }
+
+    if (NORM) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            if (i0 + r < hi) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
+        if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < SPMV_THREADS / 32; ++w) t = __dadd_rn(t, warp_sums[w]);
+            a.tile_sumsq[tile] = t;
+        }
+    }
+}
+
+Tiling tiling_of(const Matrix& m) {
+    Tiling t;
+    t.rows_per_thread = (m.bl % 2 == 0) ? 2 : 1;
+    t.tile_rows = (int64_t)SPMV_THREADS * t.rows_per_thread;
+    if (m.bl >= t.tile_rows) {
+        t.tiles_per_block = ceil_div(m.bl, t.tile_rows);
+        t.blocks_per_tile = 0;
+        t.n_tiles = m.n_blocks * t.tiles_per_block;
+    } else {
+        t.tiles_per_block = 0;
+        t.blocks_per_tile = t.tile_rows / m.bl;
+        t.n_tiles = ceil_div(m.n_blocks, t.blocks_per_tile);
+    }
+    return t;
+}
+
+template <int R, bool SCALE, bool NORM>
+static void launch_t(const SpmvArgs& a, int64_t n_tiles, cudaStream_t st) {
+    spmv_kernel<R, SCALE, NORM><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
+}
+
+template <int R>
+static void launch_r(const SpmvArgs& a, int64_t n_tiles, bool scale, bool norm, cudaStream_t st) {
+    if (scale) {
+        if (norm) launch_t<R, true, true>(a, n_tiles, st);
+        else launch_t<R, true, false>(a, n_tiles, st);
+    } else {
+        if (norm) launch_t<R, false, true>(a, n_tiles, st);
+        else launch_t<R, false, false>(a, n_tiles, st);
+    }
+}
+
+void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin,
+                 int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st) {
+    if (block_begin < 0 || block_end > m.n_blocks || block_begin > block_end)
+        fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: block range outside the matrix");
+    const Tiling t = tiling_of(m);
+    int64_t tile_begin, tile_end;
+    if (t.tiles_per_block > 0) {
+        tile_begin = block_begin * t.tiles_per_block;
+        tile_end = block_end * t.tiles_per_block;
+    } else {
+        if (block_begin % t.blocks_per_tile != 0 ||
+            (block_end % t.blocks_per_tile != 0 && block_end != m.n_blocks))
+            fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: block range not aligned to blocks_per_tile");
+        tile_begin = block_begin / t.blocks_per_tile;
+        tile_end = ceil_div(block_end, t.blocks_per_tile);
+    }
+    const int64_t n_tiles = tile_end - tile_begin;
+    if (n_tiles <= 0) return;
+    if (n_tiles > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "spmv: too many tiles for one launch");
+    SpmvArgs a;
+    a.dia_ptr = m.dia_ptr;
+    a.dia_off = m.dia_off;
+    a.seg = m.seg;
+    a.rest_rp = m.rest_rp;
+    a.rest_col = m.rest_col;
+    a.rest_val = m.rest_val;
+    a.x = x_local;
+    a.y = y;
+    a.x_scale = x_scale;
+    a.tile_sumsq = tile_sumsq;
+    a.n_rows = m.n_rows;
+    a.n_cols = m.n_cols;
+    a.row0 = m.row0;
+    a.bl = m.bl;
+    a.tiles_per_block = t.tiles_per_block;
+    a.blocks_per_tile = t.blocks_per_tile;
+    a.tile_rows = t.tile_rows;
+    a.tile_begin = tile_begin;
+    a.has_rest = m.nnz_rest > 0;
+    a.y_vec_ok = ((uintptr_t)y % 16) == 0;
+    const bool scale = x_scale != nullptr, norm = tile_sumsq != nullptr;
+    if (t.rows_per_thread == 2) launch_r<2>(a, n_tiles, scale, norm, st);
+    else launch_r<1>(a, n_tiles, scale, norm, st);
+    HDCG_LAUNCH_CHECK("spmv_kernel");
+}
+
+// ---- deterministic pairwise tree sum ------------------------------------------
+constexpr int TREE_CHUNK = 2048;
+
+__global__ void __launch_bounds__(1024) tree_chunk_kernel(const double* in, int64_t count,
+                                                          int chunk, double* out, int last) {
+    __shared__ double s[TREE_CHUNK];
+    const int64_t base = (int64_t)blockIdx.x * chunk;
+    for (int t = threadIdx.x; t < chunk; t += blockDim.x)
+        s[t] = (base + t < count) ? in[base + t] : 0.0;
+    __syncthreads();
+    for (int stride = 1; stride < chunk; stride <<= 1) {
+        for (int t = threadIdx.x * 2 * stride; t < chunk; t += blockDim.x * 2 * stride)
+            s[t] = __dadd_rn(s[t], s[t + stride]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[blockIdx.x] = s[0];
+        if (last) out[1] = 1.0 / sqrt(s[0]);
+    }
+}
+
+void tree_sum_launch(const double* vals, int64_t count, double* out, cudaStream_t st) {
+    int64_t p = 1;
+    while (p < count) p <<= 1;
+    const double* cur = vals;
+    int64_t cur_count = count;
+    double* tmp[2] = {nullptr, nullptr};
+    int which = 0;
+    while (true) {
+        const int chunk = (int)(p < TREE_CHUNK ? p : TREE_CHUNK);
+        const int64_t n_chunks = p / chunk;
+        const bool last = n_chunks == 1;
+        double* dst;
+        if (last) {
+            dst = out;
+        } else {
+            if (!tmp[which]) tmp[which] = dev_alloc<double>(n_chunks, st);
+            dst = tmp[which];
+        }
+        tree_chunk_kernel<<<(unsigned)n_chunks, 1024, 0, st>>>(cur, cur_count, chunk, dst, last);
+        HDCG_LAUNCH_CHECK("tree_chunk_kernel");
+        if (last) break;
+        cur = dst;
+        cur_count = n_chunks;
+        p = n_chunks;
+        which ^= 1;
+        if (tmp[which]) { dev_free(tmp[which], st); tmp[which] = nullptr; }
+    }
+    dev_free(tmp[0], st);
+    dev_free(tmp[1], st);
+}
+
+}  // namespace hdcg

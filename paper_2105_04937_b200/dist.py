@@ -1,0 +1,188 @@
+"""Row-slab sharding of the M-HDC SpMV across GPUs (one process per GPU).
+
+The reference has no distributed path (OpenMP only); this is
+the B200 scale-out for BASELINE config 4: contiguous z-slabs of rows, slab
+sizes a multiple of bl (so every rank's blocks are exactly global blocks and
+its conversion is bit-identical to the global one), and per SpMV one
+exchange of the x halo of width H = max|offset| with the two neighbours.
+
+Power iteration (config 4: x <- y/||y||) per step k, on rank r:
+  1. boundary blocks (rows within H of either slab edge) of y_k = A (s_{k-1} y_{k-1})
+  2. send y_k's first/last H rows to the neighbours' halo regions (NCCL P2P over
+     NVLink, torch.distributed) -- overlapped with
+  3. the interior blocks;
+  4. per-tile sums of y_i^2 (fused into the SpMV) -> local pairwise tree ->
+     all-gather of the rank roots -> top tree -> s_k = 1/sqrt(sum).
+The scale s is applied inside the next SpMV's x loads, so no separate
+normalisation pass streams y again.  Every row is owned by one rank and keeps
+its per-row operation order, so y is bitwise independent of the number of
+ranks; the tree over tiles is split into per-rank subtrees (power-of-two tile
+counts per rank) so the norm is bitwise independent of it too.
+
+The compute backend is injected: CudaSlab (libhdcgpu.so, the product) or, in
+the CPU tests only, an oracle-backed stand-in.  The transport is
+torch.distributed (NCCL on GPUs, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class SlabPlan:
+    n: int            # global rows
+    bl: int           # block width
+    halo: int         # H = max |offset|
+    world: int
+    row0: list
+    rows: list
+
+    @staticmethod
+    def make(n: int, bl: int, halo: int, world: int, unit: int | None = None) -> "SlabPlan":
+        """Contiguous slabs; boundaries are multiples of `unit` (default bl; the
+        z-plane size x bl lcm is passed for stencils so slabs are whole planes)."""
+        unit = unit or bl
+        if unit % bl:
+            raise ValueError("slab unit must be a multiple of bl")
+        n_units = (n + unit - 1) // unit
+        row0, rows = [], []
+        for r in range(world):
+            u0, u1 = r * n_units // world, (r + 1) * n_units // world
+            a, b = min(n, u0 * unit), min(n, u1 * unit)
+            row0.append(a)
+            rows.append(b - a)
+        return SlabPlan(n, bl, halo, world, row0, rows)
+
+    def boundary_blocks(self, rank: int, blocks_per_tile: int = 1):
+        """[(b0, b1), ...] block ranges that read the halo, and the interior range."""
+        rows = self.rows[rank]
+        nb = (rows + self.bl - 1) // self.bl
+        g = blocks_per_tile
+
+        def down(b):
+            return (b // g) * g
+
+        def up(b):
+            return min(nb, ((b + g - 1) // g) * g)
+
+        left = up((min(rows, self.halo) + self.bl - 1) // self.bl) if rank > 0 else 0
+        right = down(max(0, rows - self.halo) // self.bl) if rank < self.world - 1 else nb
+        if left >= right:
+            return [(0, nb)], (0, 0)
+        parts = []
+        if left > 0:
+            parts.append((0, left))
+        if right < nb:
+            parts.append((right, nb))
+        return parts, (left, right)
+
+
+class HaloExchange:
+    """x halo of a slab buffer laid out as [H left halo | rows owned | H right halo]."""
+
+    def __init__(self, plan: SlabPlan, rank: int):
+        self.plan, self.rank = plan, rank
+
+    def start(self, buf: torch.Tensor):
+        H, rows, r, p = self.plan.halo, self.plan.rows[self.rank], self.rank, self.plan.world
+        ops = []
+        if r > 0:
+            ops.append(dist.P2POp(dist.isend, buf[H:H + H], r - 1))
+            ops.append(dist.P2POp(dist.irecv, buf[0:H], r - 1))
+        if r < p - 1:
+            ops.append(dist.P2POp(dist.isend, buf[rows:rows + H], r + 1))
+            ops.append(dist.P2POp(dist.irecv, buf[H + rows:H + rows + H], r + 1))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    @staticmethod
+    def wait(reqs):
+        for q in reqs:
+            q.wait()
+
+
+def pairwise_tree(vals: torch.Tensor) -> torch.Tensor:
+    """Host-side twin of hdcg_tree_sum for tiny vectors (rank roots): pads to a
+    power of two with +0.0 and adds adjacent pairs level by level."""
+    v = vals.clone()
+    p = 1
+    while p < v.numel():
+        p <<= 1
+    if p != v.numel():
+        v = torch.cat([v, torch.zeros(p - v.numel(), dtype=v.dtype, device=v.device)])
+    while v.numel() > 1:
+        v = v[0::2] + v[1::2]
+    return v
+
+
+class SlabPowerIteration:
+    """Drives the config-4 power iteration over one rank's slab.
+
+    compute must provide: n_tiles, blocks_per_tile, n_blocks,
+      spmv(x_buf, y_buf, b0, b1, scale, tiles)   -- y_buf[H:H+rows] <- A_slab (scale * x_buf)
+      tree(tiles) -> tensor([sum, 1/sqrt(sum)])  -- deterministic pairwise tree
+    """
+
+    def __init__(self, plan: SlabPlan, rank: int, compute, x0_buf: torch.Tensor, comm=True):
+        self.plan, self.rank, self.c = plan, rank, compute
+        self.bufs = [x0_buf, torch.empty_like(x0_buf)]
+        self.bufs[1].zero_()
+        dev = x0_buf.device
+        self.scale = torch.ones(1, dtype=torch.float64, device=dev)
+        self.tiles = torch.zeros(compute.n_tiles, dtype=torch.float64, device=dev)
+        self.red = torch.zeros(2, dtype=torch.float64, device=dev)
+        self.roots = torch.zeros(plan.world, dtype=torch.float64, device=dev)
+        self.halo = HaloExchange(plan, rank)
+        self.comm = comm and plan.world > 1
+        self.parts, self.interior = plan.boundary_blocks(rank, compute.blocks_per_tile)
+
+    def step(self):
+        x, y = self.bufs
+        if not self.comm:
+            self.c.spmv(x, y, 0, self.c.n_blocks, self.scale, self.tiles)
+            red = self.c.tree(self.tiles)
+            self.scale.copy_(red[1:2])
+            self.red = red
+        else:
+            for b0, b1 in self.parts:
+                self.c.spmv(x, y, b0, b1, self.scale, self.tiles)
+            reqs = self.halo.start(y)
+            if self.interior[1] > self.interior[0]:
+                self.c.spmv(x, y, self.interior[0], self.interior[1], self.scale, self.tiles)
+            HaloExchange.wait(reqs)
+            local = self.c.tree(self.tiles)
+            dist.all_gather_into_tensor(self.roots, local[0:1].contiguous())
+            total = pairwise_tree(self.roots)[0]
+            self.red = torch.stack([total, 1.0 / torch.sqrt(total)])
+            self.scale.copy_(self.red[1:2])
+        self.bufs.reverse()
+        return self.red
+
+
+class CudaSlab:
+    """The product compute backend: libhdcgpu.so on the current CUDA stream."""
+
+    def __init__(self, matrix, halo: int):
+        from . import hdcgpu as H
+        self.H, self.m, self.halo = H, matrix, halo
+        self.n_tiles = matrix.info.n_tiles
+        self.blocks_per_tile = matrix.info.blocks_per_tile
+        self.n_blocks = matrix.n_blocks
+        self.launches = 0
+        self._out = None
+
+    def spmv(self, x_buf, y_buf, b0, b1, scale, tiles):
+        st = torch.cuda.current_stream().cuda_stream
+        self.H.spmv_slab(self.m, x_buf.data_ptr() + 8 * self.halo, y_buf.data_ptr() + 8 * self.halo,
+                         b0, b1, scale.data_ptr(), tiles.data_ptr(), st)
+        self.launches += 1
+
+    def tree(self, tiles):
+        if self._out is None:
+            self._out = torch.empty(2, dtype=torch.float64, device=tiles.device)
+        st = torch.cuda.current_stream().cuda_stream
+        self.H.tree_sum(tiles.data_ptr(), tiles.numel(), self._out.data_ptr(), st)
+        self.launches += 1 if tiles.numel() <= 2048 else 2
+        return self._out
