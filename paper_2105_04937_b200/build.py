@@ -77,7 +77,7 @@ def build_oracle(verbose=False):
     /root/reference exists (this container)."""
     targets = ["liboracle.so"]
     if os.path.isdir("/root/reference/proj/src"):
-        targets += ["ref"]
+        targets += ["ref", "shim"]
     r = subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")] + targets,
                        capture_output=not verbose, text=True)
     if r.returncode != 0:

@@ -1,0 +1,465 @@
+// hdc_gpu_shim.cpp -- drop-in GPU implementation of the reference's format-build
+// and SpMV entry points, on top of the C-ABI in include/hdcgpu.h.
+//
+// A C++ program written against the reference (proj/include/hdc/convert.hpp
+// and kernels.hpp) links this file INSTEAD OF proj/src/convert.cpp and
+// proj/src/kernels.cpp, keeps the reference's formats.cpp (the containers),
+// and links libhdcgpu.so.  Nothing else changes: same declarations, same
+// value semantics, same exception types (std::invalid_argument /
+// std::out_of_range / std::overflow_error), same synchronous behaviour
+// (y is complete when the call returns).  `workers` is accepted and ignored:
+// the GPU result is bitwise identical for every worker count, as the
+// reference guarantees for its own (kernels.hpp:24-27).
+//
+// Entry points replaced (reference file:line):
+//   DiagonalCensus::total, census_global, census_blocked   convert.cpp:32-67
+//   to_dia, to_hdc, to_mhdc                                 convert.cpp:69-169
+//   rates(HdcMatrix), rates(MHdcMatrix)                     convert.cpp:185-196
+//   BlockPlan::rows                                         kernels.cpp:33-37
+//   spmv_csr / dia / bdia / hdc / bhdc / mhdc (+ allocating) kernels.cpp:39-244
+//
+// Matrices are immutable after construction, so each one is
+// uploaded at most once: a small LRU cache maps a host matrix (its array
+// addresses, sizes and a content fingerprint) to its device handle.  Formats
+// produced by to_hdc / to_mhdc / to_dia are built on the device and
+// registered under the returned object, so their SpMVs never re-upload.
+#include <cstdint>
+#include <cstring>
+#include <list>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hdc/convert.hpp"
+#include "hdc/kernels.hpp"
+#include "hdcgpu.h"
+
+namespace hdc {
+
+namespace {
+
+[[noreturn]] void rethrow(hdcg_status s) {
+    const std::string msg = hdcg_last_error();
+    switch (s) {
+        case HDCG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case HDCG_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+        case HDCG_ERR_OVERFLOW: throw std::overflow_error(msg);
+        case HDCG_ERR_OUT_OF_MEMORY: throw std::bad_alloc();
+        default: throw std::runtime_error("hdcgpu: " + msg);
+    }
+}
+
+void call(hdcg_status s) {
+    if (s != HDCG_OK) rethrow(s);
+}
+
+// index_t is int32 in the default build; an HDC_INDEX64 build narrows here.
+struct I32View {
+    std::vector<int32_t> tmp;
+    const int32_t* ptr = nullptr;
+    explicit I32View(std::span<const index_t> s) {
+        if constexpr (sizeof(index_t) == sizeof(int32_t)) {
+            ptr = reinterpret_cast<const int32_t*>(s.data());
+        } else {
+            tmp.resize(s.size());
+            for (std::size_t k = 0; k < s.size(); ++k) {
+                if (s[k] > INT32_MAX || s[k] < INT32_MIN)
+                    throw std::overflow_error("hdcgpu: index exceeds the device index range");
+                tmp[k] = static_cast<int32_t>(s[k]);
+            }
+            ptr = tmp.data();
+        }
+    }
+};
+
+template <class T>
+std::vector<index_t> widen(const std::vector<T>& v) {
+    return std::vector<index_t>(v.begin(), v.end());
+}
+
+// ---- device cache -------------------------------------------------------------
+struct Key {
+    int kind;
+    const void* a;
+    const void* b;
+    const void* c;
+    std::size_t na, nb, nc;
+    uint64_t fp;
+    bool operator==(const Key& o) const {
+        return kind == o.kind && a == o.a && b == o.b && c == o.c && na == o.na && nb == o.nb &&
+               nc == o.nc && fp == o.fp;
+    }
+};
+
+uint64_t mix(uint64_t h, uint64_t v) {
+    h ^= v + 0x9E3779B97F4A7C15ULL + (h << 6) + (h >> 2);
+    return h;
+}
+
+template <class T>
+uint64_t fingerprint(std::span<const T> s, uint64_t h) {
+    // sizes plus a sample of the contents: guards against a freed matrix's
+    // address being reused by a different matrix of the same shape
+    h = mix(h, s.size());
+    const std::size_t n = s.size();
+    const std::size_t step = n > 64 ? n / 64 : 1;
+    for (std::size_t k = 0; k < n; k += step) {
+        uint64_t v = 0;
+        std::memcpy(&v, &s[k], sizeof(T) < 8 ? sizeof(T) : 8);
+        h = mix(h, v);
+    }
+    if (n) {
+        uint64_t v = 0;
+        std::memcpy(&v, &s[n - 1], sizeof(T) < 8 ? sizeof(T) : 8);
+        h = mix(h, v);
+    }
+    return h;
+}
+
+struct Entry {
+    Key key;
+    hdcg_matrix h;
+    int64_t bytes;
+};
+
+class Cache {
+public:
+    ~Cache() {
+        for (auto& e : lru_) hdcg_free(e.h);
+    }
+    hdcg_matrix find(const Key& k) {
+        std::lock_guard<std::mutex> lock(mu_);
+        for (auto it = lru_.begin(); it != lru_.end(); ++it)
+            if (it->key == k) {
+                lru_.splice(lru_.begin(), lru_, it);
+                return it->h;
+            }
+        return nullptr;
+    }
+    void put(const Key& k, hdcg_matrix h) {
+        hdcg_info info{};
+        hdcg_get_info(h, &info);
+        std::lock_guard<std::mutex> lock(mu_);
+        lru_.push_front(Entry{k, h, info.device_bytes});
+        bytes_ += info.device_bytes;
+        while (lru_.size() > 1 && (lru_.size() > kMaxEntries || bytes_ > kMaxBytes)) {
+            bytes_ -= lru_.back().bytes;
+            hdcg_free(lru_.back().h);
+            lru_.pop_back();
+        }
+    }
+
+private:
+    static constexpr std::size_t kMaxEntries = 256;
+    static constexpr int64_t kMaxBytes = int64_t(64) << 30;
+    std::mutex mu_;
+    std::list<Entry> lru_;
+    int64_t bytes_ = 0;
+};
+
+Cache& cache() {
+    static Cache c;
+    return c;
+}
+
+enum { K_CSR = 1, K_DIA = 2, K_HDC = 3, K_MHDC = 4 };
+
+Key key_of(const CsrMatrix& m) {
+    uint64_t fp = fingerprint(m.values(), fingerprint(m.col_ind(), fingerprint(m.row_ptr(), m.n())));
+    return Key{K_CSR, m.values().data(), m.col_ind().data(), m.row_ptr().data(), m.values().size(),
+               m.col_ind().size(), m.row_ptr().size(), fp};
+}
+Key key_of(const DiaMatrix& m) {
+    uint64_t fp = fingerprint(m.lanes(), fingerprint(m.offsets(), m.n()));
+    return Key{K_DIA, m.lanes().data(), m.offsets().data(), nullptr, m.lanes().size(), m.offsets().size(), 0, fp};
+}
+Key key_of(const HdcMatrix& m) {
+    Key d = key_of(m.dia());
+    Key c = key_of(m.csr());
+    return Key{K_HDC, d.a, d.b, c.a, d.na, d.nb, c.na, mix(d.fp, c.fp)};
+}
+Key key_of(const MHdcMatrix& m) {
+    uint64_t fp = fingerprint(m.segments(), fingerprint(m.dia_offsets(), fingerprint(m.dia_ptr(), m.bl())));
+    Key c = key_of(m.csr());
+    return Key{K_MHDC, m.segments().data(), m.dia_offsets().data(), c.a, m.segments().size(),
+               m.dia_offsets().size(), c.na, mix(fp, c.fp)};
+}
+
+hdcg_matrix device_of(const CsrMatrix& m) {
+    const Key k = key_of(m);
+    if (hdcg_matrix h = cache().find(k)) return h;
+    const I32View rp(m.row_ptr()), col(m.col_ind());
+    hdcg_matrix h = nullptr;
+    call(hdcg_build_csr(m.n(), static_cast<int64_t>(m.values().size()), rp.ptr, col.ptr, m.values().data(), 0,
+                        nullptr, &h));
+    cache().put(k, h);
+    return h;
+}
+
+hdcg_matrix upload_hdc(index_t n, std::span<const index_t> offsets, std::span<const real_t> lanes,
+                       const CsrMatrix* rest) {
+    const I32View offs(offsets);
+    hdcg_matrix h = nullptr;
+    if (rest) {
+        const I32View rp(rest->row_ptr()), col(rest->col_ind());
+        call(hdcg_upload_hdc(n, static_cast<int64_t>(offsets.size()), offs.ptr, lanes.data(), rp.ptr,
+                             static_cast<int64_t>(rest->values().size()), col.ptr, rest->values().data(), 0, &h));
+    } else {
+        std::vector<int32_t> rp(static_cast<std::size_t>(n) + 1, 0);
+        call(hdcg_upload_hdc(n, static_cast<int64_t>(offsets.size()), offs.ptr, lanes.data(), rp.data(), 0,
+                             nullptr, nullptr, 0, &h));
+    }
+    return h;
+}
+
+hdcg_matrix device_of(const DiaMatrix& m) {
+    const Key k = key_of(m);
+    if (hdcg_matrix h = cache().find(k)) return h;
+    hdcg_matrix h = upload_hdc(m.n(), m.offsets(), m.lanes(), nullptr);
+    cache().put(k, h);
+    return h;
+}
+
+hdcg_matrix device_of(const HdcMatrix& m) {
+    const Key k = key_of(m);
+    if (hdcg_matrix h = cache().find(k)) return h;
+    hdcg_matrix h = upload_hdc(m.n(), m.dia().offsets(), m.dia().lanes(), &m.csr());
+    cache().put(k, h);
+    return h;
+}
+
+hdcg_matrix device_of(const MHdcMatrix& m) {
+    const Key k = key_of(m);
+    if (hdcg_matrix h = cache().find(k)) return h;
+    const I32View dp(m.dia_ptr()), offs(m.dia_offsets()), rp(m.csr().row_ptr()), col(m.csr().col_ind());
+    hdcg_matrix h = nullptr;
+    call(hdcg_upload_mhdc(m.n(), m.bl(), dp.ptr, m.n_segments(), offs.ptr, m.segments().data(), rp.ptr,
+                          static_cast<int64_t>(m.csr().values().size()), col.ptr, m.csr().values().data(), 0, &h));
+    cache().put(k, h);
+    return h;
+}
+
+struct Exported {
+    hdcg_info info{};
+    std::vector<int32_t> dia_ptr, offsets, rest_rp, rest_col;
+    std::vector<real_t> segments, rest_val;
+};
+
+Exported export_all(hdcg_matrix h) {
+    Exported e;
+    call(hdcg_get_info(h, &e.info));
+    e.dia_ptr.resize(static_cast<std::size_t>(e.info.n_blocks) + 1);
+    e.offsets.resize(static_cast<std::size_t>(e.info.n_seg));
+    e.segments.resize(static_cast<std::size_t>(e.info.n_seg * e.info.bl));
+    e.rest_rp.resize(static_cast<std::size_t>(e.info.n_rows) + 1);
+    e.rest_col.resize(static_cast<std::size_t>(e.info.nnz_rest));
+    e.rest_val.resize(static_cast<std::size_t>(e.info.nnz_rest));
+    call(hdcg_export(h, e.dia_ptr.data(), e.offsets.data(), e.segments.data(), e.rest_rp.data(), e.rest_col.data(),
+                     e.rest_val.data()));
+    return e;
+}
+
+// Input CSR handed to the device converters.  The reference's CsrMatrix is
+// already validated by its constructor, so no HDCG_VALIDATE here.
+struct CsrArgs {
+    I32View rp, col;
+    const CsrMatrix& m;
+    explicit CsrArgs(const CsrMatrix& mm) : rp(mm.row_ptr()), col(mm.col_ind()), m(mm) {}
+};
+
+void check_theta(real_t theta, const char* what) {
+    if (!(theta >= 0.0 && theta <= 1.0)) throw std::invalid_argument(std::string(what) + ": theta must be in [0, 1]");
+}
+
+void check_vectors(index_t n, std::size_t nx, std::size_t ny, const char* what) {
+    if (nx != static_cast<std::size_t>(n) || ny != static_cast<std::size_t>(n))
+        throw std::invalid_argument(std::string(what) + ": x and y must have length n");
+}
+
+void check_plan(const BlockPlan& plan, index_t n, const char* what) {
+    if (plan.n != n || plan.bl < 1 || plan.n_blocks != (n == 0 ? 0 : (n + plan.bl - 1) / plan.bl))
+        throw std::invalid_argument(std::string(what) + ": block plan does not match matrix");
+}
+
+void run(hdcg_matrix h, index_t n, std::span<const real_t> x, std::span<real_t> y) {
+    if (n == 0) return;
+    call(hdcg_spmv_host(h, x.data(), y.data()));
+}
+
+// Create the device context when the library loads, so the first timed call
+// does not pay for it.
+struct EagerInit {
+    EagerInit() { (void)hdcg_init(0); }
+} g_eager_init;
+
+}  // namespace
+
+// ---- convert.hpp ------------------------------------------------------------------
+
+index_t DiagonalCensus::total() const {
+    index_t sum = 0;
+    for (const auto& block : per_block)
+        for (const OffsetCount& oc : block) sum += oc.count;
+    return sum;
+}
+
+static DiagonalCensus census_impl(const CsrMatrix& m, index_t bl, bool global) {
+    DiagonalCensus c;
+    c.n = m.n();
+    if (global && m.n() == 0) return c;  // convert.cpp:61-65
+    c.bl = global ? m.n() : bl;
+    c.n_blocks = m.n() == 0 ? 0 : (m.n() + c.bl - 1) / c.bl;
+    c.per_block.resize(static_cast<std::size_t>(c.n_blocks));
+    const I32View rp(m.row_ptr()), col(m.col_ind());
+    std::vector<int64_t> bp(static_cast<std::size_t>(c.n_blocks) + 1);
+    int64_t total = 0;
+    const int64_t arg_bl = global ? 0 : bl;
+    const int64_t nnz = static_cast<int64_t>(m.values().size());
+    call(hdcg_census(m.n(), nnz, rp.ptr, col.ptr, arg_bl, 0, bp.data(), nullptr, nullptr, &total));
+    std::vector<int32_t> offs(static_cast<std::size_t>(total));
+    std::vector<int64_t> cnt(static_cast<std::size_t>(total));
+    call(hdcg_census(m.n(), nnz, rp.ptr, col.ptr, arg_bl, 0, bp.data(), offs.data(), cnt.data(), &total));
+    for (index_t b = 0; b < c.n_blocks; ++b)
+        for (int64_t k = bp[b]; k < bp[b + 1]; ++k)
+            c.per_block[b].push_back(OffsetCount{static_cast<index_t>(offs[k]), static_cast<index_t>(cnt[k])});
+    return c;
+}
+
+DiagonalCensus census_blocked(const CsrMatrix& m, index_t bl) {
+    if (bl < 1) throw std::invalid_argument("census_blocked: block width must be >= 1");
+    return census_impl(m, bl, false);
+}
+
+DiagonalCensus census_global(const CsrMatrix& m) { return census_impl(m, m.n(), true); }
+
+static hdcg_matrix build_hdc_device(const CsrMatrix& m, real_t theta) {
+    const CsrArgs a(m);
+    hdcg_matrix h = nullptr;
+    call(hdcg_build_hdc(m.n(), static_cast<int64_t>(m.values().size()), a.rp.ptr, a.col.ptr, m.values().data(),
+                        theta, 0, nullptr, &h));
+    return h;
+}
+
+DiaMatrix to_dia(const CsrMatrix& m) {
+    hdcg_matrix h = build_hdc_device(m, 0.0);  // theta = 0: every populated diagonal is a lane
+    Exported e = export_all(h);
+    DiaMatrix d(m.n(), widen(e.offsets), std::move(e.segments));
+    cache().put(key_of(d), h);
+    return d;
+}
+
+HdcMatrix to_hdc(const CsrMatrix& m, real_t theta) {
+    check_theta(theta, "to_hdc");
+    hdcg_matrix h = build_hdc_device(m, theta);
+    Exported e = export_all(h);
+    HdcMatrix out(m.n(), DiaMatrix(m.n(), widen(e.offsets), std::move(e.segments)),
+                  CsrMatrix(m.n(), std::move(e.rest_val), widen(e.rest_col), widen(e.rest_rp)), theta);
+    cache().put(key_of(out), h);
+    return out;
+}
+
+MHdcMatrix to_mhdc(const CsrMatrix& m, real_t theta, index_t bl) {
+    check_theta(theta, "to_mhdc");
+    if (bl < 1) throw std::invalid_argument("to_mhdc: block width must be >= 1");
+    const CsrArgs a(m);
+    hdcg_matrix h = nullptr;
+    call(hdcg_build_mhdc(m.n(), m.n(), 0, static_cast<int64_t>(m.values().size()), a.rp.ptr, a.col.ptr,
+                         m.values().data(), theta, bl, 0, nullptr, &h));
+    Exported e = export_all(h);
+    MHdcMatrix out(m.n(), bl, widen(e.dia_ptr), widen(e.offsets), std::move(e.segments),
+                   CsrMatrix(m.n(), std::move(e.rest_val), widen(e.rest_col), widen(e.rest_rp)), theta);
+    cache().put(key_of(out), h);
+    return out;
+}
+
+static HybridRates rates_of(hdcg_matrix h) {
+    HybridRates r{};
+    int64_t slots = 0;
+    call(hdcg_rates(h, &r.alpha, &r.beta, &slots));
+    r.dia_slots = static_cast<index_t>(slots);
+    return r;
+}
+
+HybridRates rates(const HdcMatrix& m) { return rates_of(device_of(m)); }
+HybridRates rates(const MHdcMatrix& m) { return rates_of(device_of(m)); }
+
+// ---- kernels.hpp ----------------------------------------------------------------
+
+BlockPlan BlockPlan::rows(index_t n, index_t bl) {
+    if (n < 0) throw std::invalid_argument("BlockPlan: negative row count");
+    if (bl < 1) throw std::invalid_argument("BlockPlan: block width must be >= 1");
+    return BlockPlan{n, bl, n == 0 ? 0 : (n + bl - 1) / bl};
+}
+
+void spmv_csr(const CsrMatrix& m, std::span<const real_t> x, std::span<real_t> y, int) {
+    check_vectors(m.n(), x.size(), y.size(), "spmv_csr");
+    if (m.n() == 0) return;
+    run(device_of(m), m.n(), x, y);
+}
+
+void spmv_dia(const DiaMatrix& m, std::span<const real_t> x, std::span<real_t> y, int) {
+    check_vectors(m.n(), x.size(), y.size(), "spmv_dia");
+    if (m.n() == 0) return;
+    run(device_of(m), m.n(), x, y);
+}
+
+void spmv_bdia(const DiaMatrix& m, const BlockPlan& plan, std::span<const real_t> x, std::span<real_t> y, int) {
+    check_vectors(m.n(), x.size(), y.size(), "spmv_bdia");
+    check_plan(plan, m.n(), "spmv_bdia");
+    if (m.n() == 0) return;
+    run(device_of(m), m.n(), x, y);
+}
+
+void spmv_hdc(const HdcMatrix& m, std::span<const real_t> x, std::span<real_t> y, int) {
+    check_vectors(m.n(), x.size(), y.size(), "spmv_hdc");
+    if (m.n() == 0) return;
+    run(device_of(m), m.n(), x, y);
+}
+
+void spmv_bhdc(const HdcMatrix& m, const BlockPlan& plan, std::span<const real_t> x, std::span<real_t> y, int) {
+    check_vectors(m.n(), x.size(), y.size(), "spmv_bhdc");
+    check_plan(plan, m.n(), "spmv_bhdc");
+    if (m.n() == 0) return;
+    run(device_of(m), m.n(), x, y);
+}
+
+void spmv_mhdc(const MHdcMatrix& m, std::span<const real_t> x, std::span<real_t> y, int) {
+    check_vectors(m.n(), x.size(), y.size(), "spmv_mhdc");
+    if (m.n() == 0) return;
+    run(device_of(m), m.n(), x, y);
+}
+
+DenseVector spmv_csr(const CsrMatrix& m, const DenseVector& x, int w) {
+    DenseVector y(static_cast<std::size_t>(m.n()));
+    spmv_csr(m, x, y, w);
+    return y;
+}
+DenseVector spmv_dia(const DiaMatrix& m, const DenseVector& x, int w) {
+    DenseVector y(static_cast<std::size_t>(m.n()));
+    spmv_dia(m, x, y, w);
+    return y;
+}
+DenseVector spmv_bdia(const DiaMatrix& m, const BlockPlan& plan, const DenseVector& x, int w) {
+    DenseVector y(static_cast<std::size_t>(m.n()));
+    spmv_bdia(m, plan, x, y, w);
+    return y;
+}
+DenseVector spmv_hdc(const HdcMatrix& m, const DenseVector& x, int w) {
+    DenseVector y(static_cast<std::size_t>(m.n()));
+    spmv_hdc(m, x, y, w);
+    return y;
+}
+DenseVector spmv_bhdc(const HdcMatrix& m, const BlockPlan& plan, const DenseVector& x, int w) {
+    DenseVector y(static_cast<std::size_t>(m.n()));
+    spmv_bhdc(m, plan, x, y, w);
+    return y;
+}
+DenseVector spmv_mhdc(const MHdcMatrix& m, const DenseVector& x, int w) {
+    DenseVector y(static_cast<std::size_t>(m.n()));
+    spmv_mhdc(m, x, y, w);
+    return y;
+}
+
+}  // namespace hdc

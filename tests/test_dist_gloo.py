@@ -1,0 +1,147 @@
+"""Multi-process (world_size 2, gloo, CPU) coverage of the row-slab driver in
+paper_2105_04937_b200/dist.py: slab plan, boundary/interior split, halo
+exchange through torch.distributed P2P, all-gather of the norm roots, and the
+bitwise independence of y and ||y|| from the number of ranks.
+
+The SpMV itself is the CUDA kernel in production; here a test-only stand-in
+built on the oracle's M-HDC arrays computes the slab rows, reading x ONLY
+through the rank's halo'd buffer (so a wrong halo shows up as wrong bits).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2105_04937_b200 import synth
+from paper_2105_04937_b200.dist import SlabPlan, SlabPowerIteration, pairwise_tree
+
+NX, NY, NZ, BL, TILE = 16, 16, 8, 128, 64
+
+
+class OracleSlab:
+    """CPU stand-in for CudaSlab over one slab (test infrastructure)."""
+
+    def __init__(self, mh, row0, rows, halo):
+        self.mh, self.row0, self.rows, self.halo = mh, row0, rows, halo
+        self.n_blocks = (rows + BL - 1) // BL
+        self.blocks_per_tile = 1
+        self.tiles_per_block = BL // TILE
+        self.n_tiles = self.n_blocks * self.tiles_per_block
+
+    def spmv(self, x_buf, y_buf, b0, b1, scale, tiles):
+        mh, H = self.mh, self.halo
+        s = float(scale[0])
+        xb = x_buf.numpy()
+        yb = y_buf.numpy()
+        gb0 = self.row0 // BL
+        for b in range(b0, b1):
+            r0, r1 = b * BL, min((b + 1) * BL, self.rows)
+            gi = np.arange(self.row0 + r0, self.row0 + r1)
+            acc = np.zeros(r1 - r0)
+            for k, i in enumerate(gi):  # remainder, stored order
+                for e in range(mh.rest_rp[i], mh.rest_rp[i + 1]):
+                    acc[k] = acc[k] + mh.rest_val[e] * (xb[H + mh.rest_col[e] - self.row0] * s)
+            for kseg in range(mh.dia_ptr[gb0 + b], mh.dia_ptr[gb0 + b + 1]):
+                o = int(mh.offsets[kseg])
+                v = mh.segments[kseg * BL:kseg * BL + (r1 - r0)]
+                j = gi + o
+                ok = (j >= 0) & (j < mh.n)
+                xv = np.where(ok, xb[np.clip(H + j - self.row0, 0, xb.size - 1)], 0.0) * s
+                acc = np.where(ok, acc + v * xv, acc)
+            yb[H + r0:H + r1] = acc
+            for t in range(self.tiles_per_block):
+                a, c = r0 + t * TILE, min(r0 + (t + 1) * TILE, r1)
+                tiles[b * self.tiles_per_block + t] = float(np.sum(acc[a - r0:c - r0] ** 2)) if c > a else 0.0
+
+    def tree(self, tiles):
+        total = pairwise_tree(tiles)[0]
+        return torch.stack([total, 1.0 / torch.sqrt(total)])
+
+
+def _run(rank, world, port_no, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        rp, col, val = synth.laplacian7(NX, NY, NZ)
+        n = NX * NY * NZ
+        mh = Port().to_mhdc(rp, col, val, 0.6, BL)
+        halo = NX * NY
+        plan = SlabPlan.make(n, BL, halo, world, unit=NX * NY * 2)
+        row0, rows = plan.row0[rank], plan.rows[rank]
+        x = synth.x_vector(n, 5)
+        buf = torch.zeros(rows + 2 * halo, dtype=torch.float64)
+        g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
+        buf[g0 - (row0 - halo):g1 - (row0 - halo)] = torch.from_numpy(x[g0:g1])
+        comp = OracleSlab(mh, row0, rows, halo)
+        it = SlabPowerIteration(plan, rank, comp, buf, comm=True)
+        norms = []
+        for _ in range(steps):
+            red = it.step()
+            norms.append(float(red[0]))
+        y = it.bufs[0][halo:halo + rows].numpy().copy()
+        out[rank] = (row0, y, norms, plan.boundary_blocks(rank, 1))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_world(world, steps=3):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_run, args=(world, _free_port(), steps, out), nprocs=world, join=True)
+    parts = [out[r] for r in range(world)]
+    y = np.concatenate([p[1] for p in parts])
+    return y, [p[2] for p in parts], [p[3] for p in parts]
+
+
+def test_slab_plan_alignment():
+    n = 1024 * 1024 * 512
+    for p in (1, 2, 4, 8):
+        plan = SlabPlan.make(n, 4096, 1 << 20, p, unit=1 << 20)
+        assert sum(plan.rows) == n
+        assert all(r0 % (1 << 20) == 0 for r0 in plan.row0)
+        parts, interior = plan.boundary_blocks(0, 1)
+        if p > 1:
+            assert interior[1] - interior[0] == plan.rows[0] // 4096 - 256
+    small = SlabPlan.make(1000, 10, 300, 4)
+    assert sum(small.rows) == 1000 and all(r % 10 == 0 for r in small.rows)
+
+
+@pytest.mark.timeout(300)
+def test_two_ranks_bitwise_equal_one_rank():
+    y1, norms1, _ = run_world(1)
+    y2, norms2, bnds = run_world(2)
+    assert y1.tobytes() == y2.tobytes()
+    assert norms2[0] == norms2[1] == norms1[0]
+    assert bnds[0][1][1] > bnds[0][1][0]  # rank 0 has interior blocks computed under the exchange
+
+
+@pytest.mark.timeout(300)
+def test_matches_global_oracle_power_iteration():
+    """The driver + stand-in reproduce a plain global power iteration (oracle SpMV)."""
+    from oracle.oracle import Port
+    P = Port()
+    rp, col, val = synth.laplacian7(NX, NY, NZ)
+    n = NX * NY * NZ
+    mh = P.to_mhdc(rp, col, val, 0.6, BL)
+    x = synth.x_vector(n, 5)
+    s = 1.0
+    for _ in range(3):
+        y = P.spmv_mhdc(mh, x * s)
+        s = 1.0 / np.sqrt(np.dot(y, y))
+        x = y
+    y2, _, _ = run_world(2)
+    assert y2.tobytes() == y.tobytes() or np.max(np.abs(y2 - y)) <= 1e-13 * np.max(np.abs(y))
