@@ -179,6 +179,12 @@ hdcg_status hdcg_spmv_slab(hdcg_matrix m, const double* x_local, double* y, int6
                            int64_t block_end, const double* x_scale, double* tile_sumsq,
                            void* stream);
 
+/* Kernel selection (process-wide): 0 = automatic (the TMA-fed persistent kernel
+ * for even bl >= 256, the general kernel otherwise), 1 = general kernel only,
+ * 2 = TMA kernel only (ineligible shapes then fail with INVALID_ARGUMENT).
+ * Both produce bitwise identical y and tile sums; this exists for testing. */
+hdcg_status hdcg_set_kernel_policy(int policy);
+
 /* Deterministic pairwise-tree sum of vals[0..count) (padded with +0.0 to a
  * power of two): out[0] = sum, out[1] = 1/sqrt(sum).  The tree over a
  * power-of-two aligned sub-range is a subtree of the tree over the whole

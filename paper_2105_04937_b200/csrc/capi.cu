@@ -175,7 +175,10 @@ void matrix_release(Matrix* m) {
     cudaFree(m->rest_val);
     cudaFree(m->dx);
     cudaFree(m->dy);
-    if (m->host_stream) cudaStreamDestroy(m->host_stream);
+    for (cudaStream_t s : m->pipe)
+        if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : m->pipe_events)
+        if (e) cudaEventDestroy(e);
     cudaSetDevice(prev);
     delete m;
 }
@@ -518,15 +521,14 @@ hdcg_status hdcg_spmv_host(hdcg_matrix h, const double* x, double* y) {
         if (m->n_rows == 0) return;
         if (!x || !y) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: x and y must have length n");
         std::lock_guard<std::mutex> lock(g_host_mu);
-        HDCG_CUDA(cudaSetDevice(m->device));
-        if (!m->host_stream) HDCG_CUDA(cudaStreamCreateWithFlags(&m->host_stream, cudaStreamNonBlocking));
-        cudaStream_t st = m->host_stream;
-        if (!m->dx) HDCG_CUDA(cudaMalloc(&m->dx, sizeof(double) * m->n_cols));
-        if (!m->dy) HDCG_CUDA(cudaMalloc(&m->dy, sizeof(double) * m->n_rows));
-        HDCG_CUDA(cudaMemcpyAsync(m->dx, x, sizeof(double) * m->n_cols, cudaMemcpyHostToDevice, st));
-        spmv_launch(*m, m->dx + m->row0, m->dy, 0, m->n_blocks, nullptr, nullptr, st);
-        HDCG_CUDA(cudaMemcpyAsync(y, m->dy, sizeof(double) * m->n_rows, cudaMemcpyDeviceToHost, st));
-        HDCG_CUDA(cudaStreamSynchronize(st));
+        spmv_host_pipelined(m, x, y);
+    });
+}
+
+hdcg_status hdcg_set_kernel_policy(int policy) {
+    return guard([&] {
+        if (policy < 0 || policy > 2) fail(HDCG_ERR_INVALID_ARGUMENT, "kernel policy must be 0, 1 or 2");
+        g_kernel_policy = policy;
     });
 }
 

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "hdcgpu.h"
 
@@ -53,11 +54,14 @@ struct Matrix {
     int32_t* rest_rp = nullptr;
     int32_t* rest_col = nullptr;
     double* rest_val = nullptr;
-    // lazily allocated staging for hdcg_spmv_host
+    // lazily allocated state of the host-buffer SpMV pipeline (host_spmv.cu)
     double* dx = nullptr;
     double* dy = nullptr;
-    cudaStream_t host_stream = nullptr;
-    cudaEvent_t host_events[2] = {nullptr, nullptr};
+    cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
+    std::vector<cudaEvent_t> pipe_events;
+    std::vector<int64_t> chunk_blocks;  // chunk c = blocks [chunk_blocks[c], chunk_blocks[c+1])
+    std::vector<int64_t> chunk_x_hi;    // x entries [0, chunk_x_hi[c]) chunk c reads (global)
+    std::vector<int64_t> x_pieces;      // H2D pieces of x: [x_pieces[p], x_pieces[p+1])
     int64_t device_bytes = 0;
 };
 
@@ -78,6 +82,12 @@ Tiling tiling_of(const Matrix& m);
 
 void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin,
                  int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st);
+// the TMA-fed persistent kernel (spmv_tma.cu); false when the shape is not eligible
+bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin, int64_t block_end,
+                     const double* x_scale, double* tile_sumsq, cudaStream_t st);
+extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
+// synchronous SpMV on host buffers, H2D / kernel / D2H overlapped chunk by chunk
+void spmv_host_pipelined(Matrix* m, const double* x_host, double* y_host);
 void tree_sum_launch(const double* vals, int64_t count, double* out, cudaStream_t st);
 
 // ---- converters (convert.cu) ------------------------------------------------

@@ -33,6 +33,8 @@
 namespace hdcg {
 
 constexpr int SPMV_THREADS = 256;
+
+int g_kernel_policy = 0;  // 0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA only
 constexpr int REST_CHUNK = 1024;  // doubles of staged remainder products
 constexpr int SEG_UNROLL = 8;
 
@@ -187,9 +189,16 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
     }
 }
 
+// One tiling for both kernels (spmv_kernel and spmv_tma_kernel), so per-tile
+// partial sums and block-range alignment do not depend on which one runs:
+//   even bl >= 512     : 2 rows/thread, 512-row tiles, ceil(bl/512) tiles per block
+//   even bl in [256,512): 1 row/thread, 256-row tiles, 2 tiles per block
+//   even bl < 256      : 2 rows/thread, 512/bl whole blocks per tile
+//   odd bl             : 1 row/thread, 256-row tiles (or 256/bl blocks per tile)
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
-    t.rows_per_thread = (m.bl % 2 == 0) ? 2 : 1;
+    const bool even = m.bl % 2 == 0;
+    t.rows_per_thread = (even && (m.bl >= 2 * SPMV_THREADS || m.bl < SPMV_THREADS)) ? 2 : 1;
     t.tile_rows = (int64_t)SPMV_THREADS * t.rows_per_thread;
     if (m.bl >= t.tile_rows) {
         t.tiles_per_block = ceil_div(m.bl, t.tile_rows);
@@ -238,6 +247,10 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
     const int64_t n_tiles = tile_end - tile_begin;
     if (n_tiles <= 0) return;
     if (n_tiles > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "spmv: too many tiles for one launch");
+    if (g_kernel_policy != 1 &&
+        spmv_tma_launch(m, x_local, y, block_begin, block_end, x_scale, tile_sumsq, st))
+        return;
+    if (g_kernel_policy == 2) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: TMA kernel requested for an ineligible shape");
     SpmvArgs a;
     a.dia_ptr = m.dia_ptr;
     a.dia_off = m.dia_off;

@@ -44,8 +44,10 @@ EXPORTS = (
     "hdcg_last_error", "hdcg_version", "hdcg_init", "hdcg_build_mhdc", "hdcg_build_hdc",
     "hdcg_build_csr", "hdcg_upload_mhdc", "hdcg_upload_hdc", "hdcg_free", "hdcg_get_info",
     "hdcg_export", "hdcg_rates", "hdcg_census", "hdcg_spmv", "hdcg_spmv_host", "hdcg_spmv_slab",
-    "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7",
+    "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7", "hdcg_set_kernel_policy",
 )
+
+POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
 
 
 class LibraryMissing(ImportError):
@@ -103,6 +105,7 @@ def lib():
         "hdcg_spmv_host": [vp, vp, vp],
         "hdcg_spmv_slab": [vp, vp, vp, i64, i64, vp, vp, vp],
         "hdcg_tree_sum": [vp, i64, vp, vp],
+        "hdcg_set_kernel_policy": [C.c_int],
         "hdcg_gen_uniform_pm1": [C.c_uint64, C.c_uint64, i64, i64, vp, vp],
         "hdcg_gen_laplacian7": [i64, i64, i64, i64, i64, vp, vp, vp, C.POINTER(i64), vp],
     }
@@ -449,3 +452,8 @@ def gen_laplacian7(nx, ny, nz, z0, z1, rp_ptr, col_ptr, val_ptr, stream=0):
 
 def init(device: int = 0):
     check(lib().hdcg_init(device))
+
+
+def set_kernel_policy(policy: int):
+    """0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA kernel only."""
+    check(lib().hdcg_set_kernel_policy(policy))

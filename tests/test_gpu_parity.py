@@ -475,3 +475,62 @@ def test_power_iteration_matches_oracle(port):
     # iterates agree to rounding, not bitwise
     assert np.max(np.abs(yd - xs)) <= 1e-12 * np.max(np.abs(xs))
     assert abs(red[1].item() - scale) <= 1e-12 * scale
+
+
+# ---------------------------------------------------------------------------
+# the two SpMV kernels (general spmv_kernel, TMA-fed spmv_tma_kernel) agree bitwise
+
+@pytest.mark.parametrize("shape", ["lap", "quasi", "random"])
+def test_kernel_paths_bitwise_identical(port, shape):
+    rng = np.random.default_rng(11)
+    if shape == "lap":
+        rp, col, val = synth.laplacian7(40, 36, 30)
+    elif shape == "quasi":
+        rp, col, val = synth.quasi_diag(60000, 4, 300, 3000)
+    else:
+        rp, col, val = synth.random_matrix(3001, 0.003, rng)
+    n = len(rp) - 1
+    A = csr(rp, col, val)
+    x = synth.x_vector(n, 7)
+    xd = torch.from_numpy(x).cuda()
+    try:
+        for bl in (256, 300, 512, 1000, 1024, 4096, 4097, 2 * n):
+            m = H.to_mhdc(A, 0.6, bl)
+            ref = port.spmv_mhdc(port.to_mhdc(rp, col, val, 0.6, bl), x)
+            outs = []
+            for pol in (H.POLICY_GENERAL, H.POLICY_AUTO):
+                H.set_kernel_policy(pol)
+                y = torch.empty(n, dtype=torch.float64, device="cuda")
+                tiles = torch.empty(m.info.n_tiles, dtype=torch.float64, device="cuda")
+                sc = torch.tensor([0.5], dtype=torch.float64, device="cuda")
+                H.spmv_slab(m, xd.data_ptr(), y.data_ptr(), 0, m.n_blocks, sc.data_ptr(), tiles.data_ptr())
+                y2 = H.spmv_mhdc(m, x)
+                torch.cuda.synchronize()
+                outs.append((y.cpu().numpy(), tiles.cpu().numpy(), y2))
+                assert y2.tobytes() == ref.tobytes(), (shape, bl, pol)
+            assert outs[0][0].tobytes() == outs[1][0].tobytes(), (shape, bl)
+            assert outs[0][1].tobytes() == outs[1][1].tobytes(), (shape, bl)
+            if bl % 2 == 0 and bl >= 256:
+                H.set_kernel_policy(H.POLICY_TMA)
+                assert H.spmv_mhdc(m, x).tobytes() == ref.tobytes()
+            m.free()
+        h = H.to_hdc(A, 0.6)
+        refh = port.spmv_mhdc(port.to_hdc(rp, col, val, 0.6), x)
+        for pol in (H.POLICY_GENERAL, H.POLICY_AUTO):
+            H.set_kernel_policy(pol)
+            assert H.spmv_hdc(h, x).tobytes() == refh.tobytes()
+    finally:
+        H.set_kernel_policy(H.POLICY_AUTO)
+
+
+def test_tma_policy_rejects_ineligible_shape():
+    A = csr(*synth.laplacian7(8, 8, 8))
+    m = H.to_mhdc(A, 0.6, 7)
+    try:
+        H.set_kernel_policy(H.POLICY_TMA)
+        with pytest.raises(ValueError):
+            H.spmv_mhdc(m, np.ones(512))
+    finally:
+        H.set_kernel_policy(H.POLICY_AUTO)
+    with pytest.raises(ValueError):
+        H.set_kernel_policy(3)
