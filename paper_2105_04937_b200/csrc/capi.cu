@@ -354,8 +354,13 @@ hdcg_status hdcg_upload_mhdc(int64_t n, int64_t bl, const int32_t* dia_ptr, int6
             m->dia_off = upload(dia_offsets, n_seg, st);
             m->seg = upload(segments, n_seg * bl, st);
             m->rest_rp = upload(rest_row_ptr, n + 1, st);
-            m->rest_col = upload(rest_col_ind, nnz_rest, st);
-            m->rest_val = upload(rest_values, nnz_rest, st);
+            alloc_rest(m, nnz_rest, st);
+            if (nnz_rest > 0) {
+                HDCG_CUDA(cudaMemcpyAsync(m->rest_col, rest_col_ind, sizeof(int32_t) * nnz_rest,
+                                          cudaMemcpyHostToDevice, st));
+                HDCG_CUDA(cudaMemcpyAsync(m->rest_val, rest_values, sizeof(double) * nnz_rest,
+                                          cudaMemcpyHostToDevice, st));
+            }
             int64_t slots = 0, dia_nnz = 0;
             for (int64_t b = 0; b < m->n_blocks; ++b)
                 slots += (int64_t)(dia_ptr[b + 1] - dia_ptr[b]) * std::min(bl, n - b * bl);
@@ -411,8 +416,13 @@ hdcg_status hdcg_upload_hdc(int64_t n, int64_t n_diag, const int32_t* offsets, c
             m->dia_off = upload(offsets, m->n_seg, st);
             m->seg = upload(lanes, m->n_seg * m->bl, st);
             m->rest_rp = upload(rest_row_ptr, n + 1, st);
-            m->rest_col = upload(rest_col_ind, nnz_rest, st);
-            m->rest_val = upload(rest_values, nnz_rest, st);
+            alloc_rest(m, nnz_rest, st);
+            if (nnz_rest > 0) {
+                HDCG_CUDA(cudaMemcpyAsync(m->rest_col, rest_col_ind, sizeof(int32_t) * nnz_rest,
+                                          cudaMemcpyHostToDevice, st));
+                HDCG_CUDA(cudaMemcpyAsync(m->rest_val, rest_values, sizeof(double) * nnz_rest,
+                                          cudaMemcpyHostToDevice, st));
+            }
             int64_t dia_nnz = 0;
             for (int64_t k = 0; k < m->n_seg * m->bl; ++k) dia_nnz += lanes[k] != 0.0;
             m->dia_slots = m->n_seg * n;

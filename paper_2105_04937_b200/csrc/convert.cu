@@ -640,8 +640,7 @@ static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selec
     exclusive_scan(rest_cnt, m->rest_rp, in.n_rows + 1, st);
     dev_free(rest_cnt, st);
     m->nnz_rest = read_scalar(m->rest_rp + in.n_rows, st);
-    m->rest_col = dev_alloc<int32_t>(m->nnz_rest, st);
-    m->rest_val = dev_alloc<double>(m->nnz_rest, st);
+    alloc_rest(m, m->nnz_rest, st);
     if (sel.n_seg > 0 && (int64_t)sel.n_seg * bl > (int64_t)1 << 40)
         fail(HDCG_ERR_OUT_OF_MEMORY, "segments too large");
     m->seg = dev_alloc<double>(sel.n_seg * bl, st);
@@ -738,8 +737,7 @@ void build_csr(const CsrInput& in, Matrix* m, cudaStream_t st) {
     else
         HDCG_CUDA(cudaMemcpyAsync(m->rest_rp, in.row_ptr, sizeof(int32_t) * (in.n_rows + 1),
                                   cudaMemcpyDeviceToDevice, st));
-    m->rest_col = dev_alloc<int32_t>(in.nnz, st);
-    m->rest_val = dev_alloc<double>(in.nnz, st);
+    alloc_rest(m, in.nnz, st);
     if (in.nnz > 0) {
         HDCG_CUDA(cudaMemcpyAsync(m->rest_col, in.col, sizeof(int32_t) * in.nnz, cudaMemcpyDeviceToDevice, st));
         HDCG_CUDA(cudaMemcpyAsync(m->rest_val, in.val, sizeof(double) * in.nnz, cudaMemcpyDeviceToDevice, st));

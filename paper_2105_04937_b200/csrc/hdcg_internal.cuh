@@ -80,10 +80,31 @@ struct Tiling {
 };
 Tiling tiling_of(const Matrix& m);
 
+// Rows [lo, hi) of tile t (lo >= hi for the empty tail tiles of a short last block).
+__host__ __device__ inline void tile_rows(int64_t t, int64_t tiles_per_block, int64_t blocks_per_tile,
+                                          int64_t tile_rows_n, int64_t bl, int64_t n_rows, int64_t* lo,
+                                          int64_t* hi) {
+    if (tiles_per_block > 0) {
+        const int64_t b = t / tiles_per_block;
+        const int64_t b0 = b * bl;
+        const int64_t bend = b0 + bl < n_rows ? b0 + bl : n_rows;
+        *lo = b0 + (t - b * tiles_per_block) * tile_rows_n;
+        *hi = *lo + tile_rows_n < bend ? *lo + tile_rows_n : bend;
+    } else {
+        *lo = t * blocks_per_tile * bl;
+        const int64_t e = *lo + blocks_per_tile * bl;
+        *hi = e < n_rows ? e : n_rows;
+    }
+}
+
+// Launch over a tile range (both kernels); spmv_launch maps block ranges onto it.
+void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
+                       const double* x_scale, double* tile_sumsq, cudaStream_t st);
+
 void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin,
                  int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st);
 // the TMA-fed persistent kernel (spmv_tma.cu); false when the shape is not eligible
-bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin, int64_t block_end,
+bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st);
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
 // synchronous SpMV on host buffers, H2D / kernel / D2H overlapped chunk by chunk
@@ -121,6 +142,16 @@ T* dev_alloc(int64_t count, cudaStream_t st) {
 template <class T>
 void dev_free(T* p, cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
+}
+
+// Remainder arrays carry REST_PAD zeroed entries past the end so the TMA kernel
+// can move 16-byte aligned windows that run over the last entry.
+constexpr int64_t REST_PAD = 8;
+inline void alloc_rest(Matrix* m, int64_t nnz, cudaStream_t st) {
+    m->rest_col = dev_alloc<int32_t>(nnz + REST_PAD, st);
+    m->rest_val = dev_alloc<double>(nnz + REST_PAD, st);
+    HDCG_CUDA(cudaMemsetAsync(m->rest_col + nnz, 0, sizeof(int32_t) * REST_PAD, st));
+    HDCG_CUDA(cudaMemsetAsync(m->rest_val + nnz, 0, sizeof(double) * REST_PAD, st));
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

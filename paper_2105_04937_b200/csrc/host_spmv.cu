@@ -22,52 +22,57 @@ namespace {
 
 constexpr int PIPE_CHUNKS = 8;
 
-// per block: highest global column any of its rows reads (-1: none)
-__global__ void block_xhi_kernel(int64_t n_blocks, int64_t bl, int64_t n_rows, int64_t row0, int64_t n_cols,
-                                 const int32_t* dia_ptr, const int32_t* dia_off, const int32_t* rest_rp,
-                                 const int32_t* rest_col, int64_t* hi_out) {
+// per tile: highest global column any of its rows reads (-1: none)
+__global__ void tile_xhi_kernel(int64_t n_tiles, int64_t tpb, int64_t bpt, int64_t tile_rows_n, int64_t bl,
+                                int64_t n_rows, int64_t row0, int64_t n_cols, const int32_t* dia_ptr,
+                                const int32_t* dia_off, const int32_t* rest_rp, const int32_t* rest_col,
+                                int64_t* hi_out) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t b = warp; b < n_blocks; b += n_warps) {
-        const int64_t r0 = b * bl, r1 = min(r0 + bl, n_rows);
+    for (int64_t t = warp; t < n_tiles; t += n_warps) {
+        int64_t lo, hi_row;
+        tile_rows(t, tpb, bpt, tile_rows_n, bl, n_rows, &lo, &hi_row);
         int64_t hi = -1;
-        if (lane == 0) {
-            const int k0 = dia_ptr[b], k1 = dia_ptr[b + 1];
-            if (k1 > k0) hi = min(n_cols - 1, row0 + r1 - 1 + (int64_t)dia_off[k1 - 1]);
-        }
-        if (rest_rp) {
-            const int64_t e0 = rest_rp[r0], e1 = rest_rp[r1];
-            for (int64_t e = e0 + lane; e < e1; e += 32) hi = max(hi, (int64_t)rest_col[e]);
+        if (lo < hi_row) {
+            // segments: the last block of the tile has the largest rows; offsets ascend per block
+            for (int64_t b = lo / bl + lane; b <= (hi_row - 1) / bl; b += 32) {
+                const int k0 = dia_ptr[b], k1 = dia_ptr[b + 1];
+                const int64_t last_row = min(hi_row, (b + 1) * bl) - 1;
+                if (k1 > k0) hi = max(hi, min(n_cols - 1, row0 + last_row + (int64_t)dia_off[k1 - 1]));
+            }
+            if (rest_rp) {
+                const int64_t e0 = rest_rp[lo], e1 = rest_rp[hi_row];
+                for (int64_t e = e0 + lane; e < e1; e += 32) hi = max(hi, (int64_t)rest_col[e]);
+            }
         }
         for (int o = 16; o > 0; o >>= 1) hi = max(hi, (int64_t)__shfl_down_sync(0xffffffffu, hi, o));
-        if (lane == 0) hi_out[b] = hi;
+        if (lane == 0) hi_out[t] = hi;
     }
 }
 
 void plan_pipeline(Matrix* m, cudaStream_t st) {
     const Tiling t = tiling_of(*m);
-    const int64_t align = t.blocks_per_tile > 0 ? t.blocks_per_tile : 1;
-    const int64_t nb = m->n_blocks;
-    int64_t per = std::max<int64_t>(align, ceil_div(ceil_div(nb, PIPE_CHUNKS), align) * align);
-    m->chunk_blocks.clear();
-    for (int64_t b = 0; b < nb; b += per) m->chunk_blocks.push_back(b);
-    m->chunk_blocks.push_back(nb);
+    const int64_t nt = t.n_tiles;
+    const int64_t per = std::max<int64_t>(1, ceil_div(nt, PIPE_CHUNKS));
+    m->chunk_blocks.clear();  // holds TILE boundaries of the chunks
+    for (int64_t q = 0; q < nt; q += per) m->chunk_blocks.push_back(q);
+    m->chunk_blocks.push_back(nt);
     const int64_t n_chunks = (int64_t)m->chunk_blocks.size() - 1;
 
-    std::vector<int64_t> hi((size_t)nb);
-    int64_t* d_hi = dev_alloc<int64_t>(nb, st);
-    block_xhi_kernel<<<grid_cap(ceil_div(nb * 32, 256)), 256, 0, st>>>(
-        nb, m->bl, m->n_rows, m->row0, m->n_cols, m->dia_ptr, m->dia_off, m->nnz_rest > 0 ? m->rest_rp : nullptr,
-        m->rest_col, d_hi);
-    HDCG_LAUNCH_CHECK("block_xhi_kernel");
-    HDCG_CUDA(cudaMemcpyAsync(hi.data(), d_hi, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, st));
+    std::vector<int64_t> hi((size_t)nt);
+    int64_t* d_hi = dev_alloc<int64_t>(nt, st);
+    tile_xhi_kernel<<<grid_cap(ceil_div(nt * 32, 256)), 256, 0, st>>>(
+        nt, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, m->row0, m->n_cols, m->dia_ptr,
+        m->dia_off, m->nnz_rest > 0 ? m->rest_rp : nullptr, m->rest_col, d_hi);
+    HDCG_LAUNCH_CHECK("tile_xhi_kernel");
+    HDCG_CUDA(cudaMemcpyAsync(hi.data(), d_hi, sizeof(int64_t) * nt, cudaMemcpyDeviceToHost, st));
     HDCG_CUDA(cudaStreamSynchronize(st));
     dev_free(d_hi, st);
     m->chunk_x_hi.assign((size_t)n_chunks, 0);
     int64_t run = 0;  // chunks run in order, so the requirement is cumulative
     for (int64_t c = 0; c < n_chunks; ++c) {
-        for (int64_t b = m->chunk_blocks[c]; b < m->chunk_blocks[c + 1]; ++b) run = std::max(run, hi[b] + 1);
+        for (int64_t q = m->chunk_blocks[c]; q < m->chunk_blocks[c + 1]; ++q) run = std::max(run, hi[q] + 1);
         m->chunk_x_hi[c] = run;
     }
     // x pieces: equal slices of [0, n_cols), 16-byte aligned boundaries
@@ -109,11 +114,15 @@ void spmv_host_pipelined(Matrix* m, const double* x, double* y) {
             HDCG_CUDA(cudaStreamWaitEvent(s_k, ev_in[p], 0));
             p_done = p;
         }
-        const int64_t b0 = m->chunk_blocks[c], b1 = m->chunk_blocks[c + 1];
-        spmv_launch(*m, m->dx + m->row0, m->dy, b0, b1, nullptr, nullptr, s_k);
+        const int64_t q0 = m->chunk_blocks[c], q1 = m->chunk_blocks[c + 1];
+        spmv_launch_tiles(*m, m->dx + m->row0, m->dy, q0, q1, nullptr, nullptr, s_k);
         HDCG_CUDA(cudaEventRecord(ev_k[c], s_k));
         HDCG_CUDA(cudaStreamWaitEvent(s_out, ev_k[c], 0));
-        const int64_t r0 = b0 * m->bl, r1 = std::min(b1 * m->bl, m->n_rows);
+        int64_t r0, r1, dummy;
+        const Tiling t = tiling_of(*m);
+        tile_rows(q0, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &r0, &dummy);
+        tile_rows(q1 - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &dummy, &r1);
+        r0 = std::min(r0, m->n_rows);
         if (r1 > r0)
             HDCG_CUDA(cudaMemcpyAsync(y + r0, m->dy + r0, sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost, s_out));
     }

@@ -244,11 +244,18 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
         tile_begin = block_begin / t.blocks_per_tile;
         tile_end = ceil_div(block_end, t.blocks_per_tile);
     }
+    spmv_launch_tiles(m, x_local, y, tile_begin, tile_end, x_scale, tile_sumsq, st);
+}
+
+void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
+                       const double* x_scale, double* tile_sumsq, cudaStream_t st) {
+    const Tiling t = tiling_of(m);
+    if (tile_begin < 0 || tile_end > t.n_tiles || tile_begin > tile_end)
+        fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: tile range outside the matrix");
     const int64_t n_tiles = tile_end - tile_begin;
     if (n_tiles <= 0) return;
-    if (n_tiles > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "spmv: too many tiles for one launch");
-    if (g_kernel_policy != 1 &&
-        spmv_tma_launch(m, x_local, y, block_begin, block_end, x_scale, tile_sumsq, st))
+    if (tile_end > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "spmv: too many tiles for one launch");
+    if (g_kernel_policy != 1 && spmv_tma_launch(m, x_local, y, tile_begin, tile_end, x_scale, tile_sumsq, st))
         return;
     if (g_kernel_policy == 2) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: TMA kernel requested for an ineligible shape");
     SpmvArgs a;

@@ -3,25 +3,28 @@
 // Same arithmetic as spmv.cu (the reference's per-row order, kernels.cpp:173-206,
 // __dmul_rn/__dadd_rn, bitwise equal), different data movement:
 //
-//   * persistent grid (148 SMs x CTAS_PER_SM CTAs); CTA c owns tiles
-//     c, c+grid, ...; a tile is TILE = 256*R rows inside one row block;
-//   * warp 8 is the producer: one elected lane streams every (tile, segment)
-//     slice -- TILE contiguous doubles of segment k -- global -> shared with
-//     cp.async.bulk (the 1-D TMA path, UBLKCP in SASS) into an NSTAGE-deep ring,
-//     completion signalled through mbarrier transaction counts, L2 evict-first
-//     (segment values are read exactly once);
-//   * warps 0-7 consume: per segment they wait on the stage's full barrier, read
-//     their R slots with one 8/16-byte shared load, multiply with x (issued
-//     ahead, per group of up to XGROUP segments, through the L1/tex path where
-//     the near offsets of a tile share lines and the far ones hit L2), add in
-//     stored order and release the stage;
-//   * the producer runs up to NSTAGE slices (NSTAGE*TILE*8 bytes, 64 KB) ahead
-//     of the consumers, across tile boundaries, so every SM keeps ~200 KB of
-//     segment traffic in flight with a handful of instructions per 4 KB;
-//   * y is stored once per tile (streaming store); the optional fused
-//     sum-of-squares per tile uses the same fixed reduction order as spmv.cu.
-// Used for even bl >= TILE (all BASELINE M-HDC configurations and HDC with
-// even n); other shapes take the general kernel in spmv.cu.
+//   * persistent grid (SMs x CTAs/SM); CTA c owns tiles c, c+grid, ... of the
+//     shared tiling (tiling_of: TILE = 256*R rows inside one row block);
+//   * warp 8 is the producer: one lane streams, per tile,
+//       - the tile's CSR remainder (col_ind and values of rows [lo, hi), in
+//         chunks of REST_CHUNK entries, 16-byte aligned windows) into a
+//         2-stage "rest" ring, then
+//       - every (tile, segment) slice -- TILE contiguous doubles of segment k --
+//         into an NSTAGE-deep "segment" ring,
+//     with cp.async.bulk (the 1-D TMA path, UBLKCP in SASS), completion through
+//     mbarrier transaction counts, L2 evict-first (everything it moves is read once);
+//   * warps 0-7 consume in the reference's order: remainder products (x gathered
+//     through L1/L2) written back in place in shared memory, per-row sequential
+//     sums, then per segment: wait for the slice, read the thread's R slots,
+//     multiply with x (issued ahead per group of XGROUP segments), add, release;
+//   * the producer runs up to NSTAGE slices + 2 remainder chunks ahead of the
+//     consumers, across tile boundaries, so each SM keeps well over 100 KB of
+//     matrix traffic in flight at a few instructions per 4 KB;
+//   * y is stored once per tile (streaming store); the optional fused per-tile
+//     sum of squares has the same fixed reduction order as spmv.cu, with one
+//     consumer barrier per tile (double-buffered warp partials).
+// Used for even bl >= 256 (all BASELINE M-HDC configurations, HDC with even n);
+// other shapes take the general kernel in spmv.cu.
 #include "hdcg_internal.cuh"
 
 namespace hdcg {
@@ -31,9 +34,9 @@ namespace {
 constexpr int CONSUMER_WARPS = 8;
 constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
-constexpr int NSTAGE = 16;
 constexpr int XGROUP = 8;
-constexpr int REST_CHUNK_T = 1024;
+constexpr int REST_CHUNK = 1024;  // entries per remainder stage (multiple of 4)
+constexpr int REST_STAGES = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -79,7 +82,7 @@ struct TmaArgs {
     const int32_t* dia_off;
     const double* seg;
     const int32_t* rest_rp;
-    const int32_t* rest_col;
+    const int32_t* rest_col;  // padded: readable up to a multiple of 4 entries past nnz_rest
     const double* rest_val;
     const double* x;
     double* y;
@@ -88,18 +91,19 @@ struct TmaArgs {
     int64_t n_rows, n_cols, row0, bl;
     int tiles_per_block;
     int tile_begin, tile_end;
+    int nstage;
     int has_rest;
     int y_vec_ok;
 };
 
-struct TileGeo {
+struct Geo {
     int64_t lo, hi, b0;
     int b;
 };
 
 template <int R>
-__device__ __forceinline__ TileGeo tile_geo(const TmaArgs& a, int tile) {
-    TileGeo g;
+__device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
+    Geo g;
     g.b = tile / a.tiles_per_block;
     const int t = tile - g.b * a.tiles_per_block;
     g.b0 = (int64_t)g.b * a.bl;
@@ -109,22 +113,52 @@ __device__ __forceinline__ TileGeo tile_geo(const TmaArgs& a, int tile) {
     return g;
 }
 
+struct Smem {
+    double* ring;      // nstage * TILE
+    int32_t* rcol;     // REST_STAGES * REST_CHUNK
+    double* rval;      // REST_STAGES * REST_CHUNK
+    double* wsum;      // 2 * CONSUMER_WARPS
+    uint64_t* full;    // nstage
+    uint64_t* empty;   // nstage
+    uint64_t* rfull;   // REST_STAGES
+    uint64_t* rempty;  // REST_STAGES
+};
+
+__host__ __device__ inline size_t smem_bytes(int R, int nstage) {
+    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + REST_STAGES * REST_CHUNK + 2 * CONSUMER_WARPS) +
+           sizeof(int32_t) * REST_STAGES * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
+}
+
+__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage) {
+    Smem s;
+    s.ring = reinterpret_cast<double*>(base);
+    s.rval = s.ring + (size_t)nstage * CONSUMERS * R;
+    s.wsum = s.rval + REST_STAGES * REST_CHUNK;
+    s.rcol = reinterpret_cast<int32_t*>(s.wsum + 2 * CONSUMER_WARPS);
+    s.full = reinterpret_cast<uint64_t*>(s.rcol + REST_STAGES * REST_CHUNK);
+    s.empty = s.full + nstage;
+    s.rfull = s.empty + nstage;
+    s.rempty = s.rfull + REST_STAGES;
+    return s;
+}
+
 template <int R, bool SCALE, bool NORM>
 __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* ring = reinterpret_cast<double*>(smem_raw);                       // NSTAGE * TILE
-    double* prod = ring + NSTAGE * TILE;                                      // REST_CHUNK_T
-    double* warp_sums = prod + REST_CHUNK_T;                                  // CONSUMER_WARPS
-    uint64_t* full = reinterpret_cast<uint64_t*>(warp_sums + CONSUMER_WARPS);  // NSTAGE
-    uint64_t* empty = full + NSTAGE;                                          // NSTAGE
+    const Smem S = carve(smem_raw, R, a.nstage);
+    const int NS = a.nstage;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CONSUMER_WARPS);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&S.full[s], 1);
+            mbar_init(&S.empty[s], CONSUMER_WARPS);
+        }
+        for (int s = 0; s < REST_STAGES; ++s) {
+            mbar_init(&S.rfull[s], 1);
+            mbar_init(&S.rempty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -134,18 +168,32 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
         const uint64_t policy = evict_first_policy();
-        uint32_t it = 0;
+        uint32_t it = 0, rit = 0;
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-            const TileGeo g = tile_geo<R>(a, tile);
+            const Geo g = geo<R>(a, tile);
             if (g.lo >= g.hi) continue;
+            if (a.has_rest) {
+                const int64_t e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
+                if (e_lo < e_hi) {
+                    const int64_t A = e_lo & ~int64_t(3), E = (e_hi + 3) & ~int64_t(3);
+                    for (int64_t c = A; c < E; c += REST_CHUNK, ++rit) {
+                        const int cnt = (int)min((int64_t)REST_CHUNK, E - c);
+                        const int s = rit % REST_STAGES;
+                        if (rit >= REST_STAGES) mbar_wait(&S.rempty[s], ((rit / REST_STAGES) - 1) & 1);
+                        mbar_expect_tx(&S.rfull[s], (uint32_t)cnt * 12u);
+                        bulk_g2s(S.rcol + s * REST_CHUNK, a.rest_col + c, (uint32_t)cnt * 4u, &S.rfull[s], policy);
+                        bulk_g2s(S.rval + s * REST_CHUNK, a.rest_val + c, (uint32_t)cnt * 8u, &S.rfull[s], policy);
+                    }
+                }
+            }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
             const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
             for (int k = k0; k < k1; ++k, ++it, src += a.bl) {
-                const int s = it % NSTAGE;
-                if (it >= NSTAGE) mbar_wait(&empty[s], ((it / NSTAGE) - 1) & 1);
-                mbar_expect_tx(&full[s], bytes);
-                bulk_g2s(ring + s * TILE, src, bytes, &full[s], policy);
+                const int s = it % NS;
+                if (it >= (uint32_t)NS) mbar_wait(&S.empty[s], ((it / NS) - 1) & 1);
+                mbar_expect_tx(&S.full[s], bytes);
+                bulk_g2s(S.ring + s * TILE, src, bytes, &S.full[s], policy);
             }
         }
         return;
@@ -154,9 +202,9 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     // -------------------------------- consumers --------------------------------
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
-    uint32_t it = 0;
+    uint32_t it = 0, rit = 0, par = 0;
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-        const TileGeo g = tile_geo<R>(a, tile);
+        const Geo g = geo<R>(a, tile);
         if (g.lo >= g.hi) {
             if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
             continue;
@@ -167,31 +215,40 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-        // CSR remainder first (stored order), products staged through smem
+        // CSR remainder first (stored order): products in place, then per-row sums
         if (a.has_rest) {
-            const int64_t e_lo = a.rest_rp[g.lo], e_hi = a.rest_rp[g.hi];
+            const int64_t e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
             if (e_lo < e_hi) {
                 int64_t kb[R], ke[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const bool ok = i0 + r < g.hi;
-                    kb[r] = ok ? a.rest_rp[i0 + r] : 0;
-                    ke[r] = ok ? a.rest_rp[i0 + r + 1] : 0;
+                    kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
+                    ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
                 }
-                for (int64_t c0 = e_lo; c0 < e_hi; c0 += REST_CHUNK_T) {
-                    const int64_t c1 = min(c0 + (int64_t)REST_CHUNK_T, e_hi);
-                    for (int64_t e = c0 + threadIdx.x; e < c1; e += CONSUMERS) {
-                        double xv = __ldg(a.x + ((int64_t)__ldcs(a.rest_col + e) - a.row0));
+                const int64_t A = e_lo & ~int64_t(3), E = (e_hi + 3) & ~int64_t(3);
+                for (int64_t c = A; c < E; c += REST_CHUNK, ++rit) {
+                    const int s = rit % REST_STAGES;
+                    mbar_wait(&S.rfull[s], (rit / REST_STAGES) & 1);
+                    int32_t* cs = S.rcol + s * REST_CHUNK;
+                    double* vs = S.rval + s * REST_CHUNK;
+                    const int64_t q0 = max(c, e_lo), q1 = min(c + REST_CHUNK, e_hi);
+                    for (int64_t q = q0 + threadIdx.x; q < q1; q += CONSUMERS) {
+                        const int e = (int)(q - c);
+                        double xv = __ldg(a.x + ((int64_t)cs[e] - a.row0));
                         if (SCALE) xv = __dmul_rn(xv, sc);
-                        prod[e - c0] = __dmul_rn(__ldcs(a.rest_val + e), xv);
+                        vs[e] = __dmul_rn(vs[e], xv);
                     }
+                    // order these generic-proxy writes before the TMA refill of the stage
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     consumer_sync();
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int64_t q0 = max(kb[r], c0), q1 = min(ke[r], c1);
-                        for (int64_t q = q0; q < q1; ++q) acc[r] = __dadd_rn(acc[r], prod[q - c0]);
+                        const int64_t p0 = max(kb[r], c), p1 = min(ke[r], c + REST_CHUNK);
+                        for (int64_t p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], vs[p - c]);
                     }
                     consumer_sync();
+                    if (threadIdx.x == 0) mbar_arrive(&S.rempty[s]);
                 }
             }
         }
@@ -225,9 +282,9 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
             for (int u = 0; u < XGROUP; ++u) {
                 if (kg + u >= k1) break;
-                const int s = it % NSTAGE;
-                mbar_wait(&full[s], (it / NSTAGE) & 1);
-                const double* st = ring + s * TILE + R * threadIdx.x;
+                const int s = it % NS;
+                mbar_wait(&S.full[s], (it / NS) & 1);
+                const double* st = S.ring + s * TILE + R * threadIdx.x;
                 double v[R];
                 if (R == 2) {
                     const double2 t = *reinterpret_cast<const double2*>(st);
@@ -237,7 +294,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                     v[0] = st[0];
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+                if (lane == 0) mbar_arrive(&S.empty[s]);
                 ++it;
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -264,51 +321,40 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                 if (i0 + r < g.hi) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
-            if (lane == 0) warp_sums[warp] = s;
+            double* ws = S.wsum + par * CONSUMER_WARPS;
+            if (lane == 0) ws[warp] = s;
             consumer_sync();
             if (threadIdx.x == 0) {
                 double t = 0.0;
 #pragma unroll
-                for (int w = 0; w < CONSUMER_WARPS; ++w) t = __dadd_rn(t, warp_sums[w]);
+                for (int w = 0; w < CONSUMER_WARPS; ++w) t = __dadd_rn(t, ws[w]);
                 a.tile_sumsq[tile] = t;
             }
-            consumer_sync();
+            par ^= 1;  // the next tile writes the other buffer; its barrier orders this read
         }
     }
 }
 
-template <int R>
-constexpr size_t smem_bytes() {
-    return sizeof(double) * (NSTAGE * CONSUMERS * R + REST_CHUNK_T + CONSUMER_WARPS) + sizeof(uint64_t) * 2 * NSTAGE;
-}
-
 template <int R, bool SCALE, bool NORM>
-void launch_one(const TmaArgs& a, int grid, cudaStream_t st) {
+void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM>;
-    static bool configured = false;  // per instantiation; attribute set once per process
-    if (!configured) {
-        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<R>()));
-        configured = true;
+    static size_t configured = 0;  // per instantiation
+    if (configured < smem) {
+        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(R, 32)));
+        configured = smem_bytes(R, 32);
     }
-    k<<<grid, THREADS, smem_bytes<R>(), st>>>(a);
+    k<<<grid, THREADS, smem, st>>>(a);
 }
 
 template <int R>
-void launch_r(const TmaArgs& a, int grid, bool scale, bool norm, cudaStream_t st) {
+void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if (scale) {
-        if (norm) launch_one<R, true, true>(a, grid, st);
-        else launch_one<R, true, false>(a, grid, st);
+        if (norm) launch_one<R, true, true>(a, grid, smem, st);
+        else launch_one<R, true, false>(a, grid, smem, st);
     } else {
-        if (norm) launch_one<R, false, true>(a, grid, st);
-        else launch_one<R, false, false>(a, grid, st);
+        if (norm) launch_one<R, false, true>(a, grid, smem, st);
+        else launch_one<R, false, false>(a, grid, smem, st);
     }
-}
-
-int ctas_per_sm(int rows_per_thread) {
-    // smem-limited: 228 KB per SM, ~1 KB reserved per CTA
-    const size_t per = (rows_per_thread == 2 ? smem_bytes<2>() : smem_bytes<1>()) + 1024;
-    int c = (int)((228 * 1024) / per);
-    return c < 1 ? 1 : (c > 4 ? 4 : c);
 }
 
 int sm_count() {
@@ -324,18 +370,15 @@ int sm_count() {
 
 }  // namespace
 
-// Eligible shapes: even bl >= 256 (tile rows 256 or 512), 16-byte aligned
-// segment storage.  Returns false when the general kernel must be used.
-bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin, int64_t block_end,
+bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st) {
     if (m.bl % 2 != 0 || m.bl < CONSUMERS) return false;
     if (m.n_seg > 0 && ((uintptr_t)m.seg % 16) != 0) return false;
-    const int R = m.bl >= 2 * CONSUMERS ? 2 : 1;
-    const int64_t tile_rows = (int64_t)CONSUMERS * R;
-    const int64_t tpb = ceil_div(m.bl, tile_rows);
-    const int64_t t0 = block_begin * tpb, t1 = block_end * tpb;
-    if (t1 > 0x7fffffffLL) return false;
-    if (t1 <= t0) return true;
+    if (m.nnz_rest > 0 && (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0)) return false;
+    const Tiling t = tiling_of(m);
+    const int R = t.rows_per_thread;
+    if (t.tiles_per_block <= 0 || t.tile_rows != (int64_t)CONSUMERS * R) return false;
+    if (tile_end <= tile_begin) return true;
     TmaArgs a;
     a.dia_ptr = m.dia_ptr;
     a.dia_off = m.dia_off;
@@ -351,16 +394,20 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.n_cols = m.n_cols;
     a.row0 = m.row0;
     a.bl = m.bl;
-    a.tiles_per_block = (int)tpb;
-    a.tile_begin = (int)t0;
-    a.tile_end = (int)t1;
+    a.tiles_per_block = (int)t.tiles_per_block;
+    a.tile_begin = (int)tile_begin;
+    a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
-    const int64_t n_tiles = t1 - t0;
-    const int64_t cap = (int64_t)sm_count() * ctas_per_sm(R);
+    // ring depth: ~64 KB of segment slices, half that when a remainder ring is also needed
+    a.nstage = (a.has_rest ? 16 : 32) / R;
+    const size_t smem = smem_bytes(R, a.nstage);
+    const int per_sm = (int)std::min<size_t>(3, (227 * 1024) / (smem + 1024));
+    const int64_t n_tiles = tile_end - tile_begin;
+    const int64_t cap = (int64_t)sm_count() * std::max(1, per_sm);
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
-    if (R == 2) launch_r<2>(a, grid, x_scale != nullptr, tile_sumsq != nullptr, st);
-    else launch_r<1>(a, grid, x_scale != nullptr, tile_sumsq != nullptr, st);
+    if (R == 2) launch_r<2>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
+    else launch_r<1>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
     HDCG_LAUNCH_CHECK("spmv_tma_kernel");
     return true;
 }

@@ -6,6 +6,9 @@ row_ptr/col/values); y bitwise equal (stricter than BASELINE.json's
 1e-12 * sum|a_ij x_j| per row, which is also asserted where the oracle is a
 different summation order).
 """
+import os
+import subprocess
+
 import numpy as np
 import pytest
 
@@ -534,3 +537,21 @@ def test_tma_policy_rejects_ineligible_shape():
         H.set_kernel_policy(H.POLICY_AUTO)
     with pytest.raises(ValueError):
         H.set_kernel_policy(3)
+
+
+# ---------------------------------------------------------------------------
+# the drop-in: the reference's OWN acceptance program, linked against the shim
+
+ACCEPT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "acceptance_gpu")
+
+
+@pytest.mark.skipif(not os.path.exists(ACCEPT), reason="acceptance_gpu not built (needs /root/reference at build time)")
+def test_reference_acceptance_through_gpu_shim():
+    """proj/tests/acceptance.cpp compiled unchanged against formats.cpp + our shim
+    (replacing convert.cpp and kernels.cpp) + libhdcgpu.so: all 8 criteria pass,
+    including criterion 2 (209 matrices x 6 kernels vs the dense oracle, worker
+    invariance) and criterion 1's bit-exact fixtures."""
+    r = subprocess.run([ACCEPT], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(ACCEPT))
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all 8 criteria passed" in r.stdout
