@@ -25,6 +25,9 @@
 //     consumer barrier per tile (double-buffered warp partials).
 // Used for even bl >= 256 (all BASELINE M-HDC configurations, HDC with even n);
 // other shapes take the general kernel in spmv.cu.
+#include <algorithm>
+#include <cstdlib>
+
 #include "hdcg_internal.cuh"
 
 namespace hdcg {
@@ -124,18 +127,19 @@ struct Smem {
     uint64_t* rempty;  // REST_STAGES
 };
 
-__host__ __device__ inline size_t smem_bytes(int R, int nstage) {
-    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + REST_STAGES * REST_CHUNK + 2 * CONSUMER_WARPS) +
-           sizeof(int32_t) * REST_STAGES * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
+// rest_stages is 0 for matrices without a remainder (no ring reserved: keeps 3 CTAs/SM)
+__host__ __device__ inline size_t smem_bytes(int R, int nstage, int rest_stages) {
+    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
+           sizeof(int32_t) * rest_stages * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
 }
 
-__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage) {
+__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int rest_stages) {
     Smem s;
     s.ring = reinterpret_cast<double*>(base);
     s.rval = s.ring + (size_t)nstage * CONSUMERS * R;
-    s.wsum = s.rval + REST_STAGES * REST_CHUNK;
+    s.wsum = s.rval + rest_stages * REST_CHUNK;
     s.rcol = reinterpret_cast<int32_t*>(s.wsum + 2 * CONSUMER_WARPS);
-    s.full = reinterpret_cast<uint64_t*>(s.rcol + REST_STAGES * REST_CHUNK);
+    s.full = reinterpret_cast<uint64_t*>(s.rcol + rest_stages * REST_CHUNK);
     s.empty = s.full + nstage;
     s.rfull = s.empty + nstage;
     s.rempty = s.rfull + REST_STAGES;
@@ -146,7 +150,7 @@ template <int R, bool SCALE, bool NORM>
 __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const Smem S = carve(smem_raw, R, a.nstage);
+    const Smem S = carve(smem_raw, R, a.nstage, a.has_rest ? REST_STAGES : 0);
     const int NS = a.nstage;
 
     const int warp = threadIdx.x >> 5;
@@ -340,8 +344,9 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM>;
     static size_t configured = 0;  // per instantiation
     if (configured < smem) {
-        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(R, 32)));
-        configured = smem_bytes(R, 32);
+        const size_t cap = smem_bytes(R, 32, REST_STAGES);
+        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+        configured = cap;
     }
     k<<<grid, THREADS, smem, st>>>(a);
 }
@@ -401,8 +406,13 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
     // ring depth: ~64 KB of segment slices, half that when a remainder ring is also needed
     a.nstage = (a.has_rest ? 16 : 32) / R;
-    const size_t smem = smem_bytes(R, a.nstage);
-    const int per_sm = (int)std::min<size_t>(3, (227 * 1024) / (smem + 1024));
+    // tuning knobs for profiling sweeps (not needed in normal use)
+    static const int env_stage_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
+    static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
+    if (env_stage_kb > 0) a.nstage = std::max(2, std::min(32, env_stage_kb / (2 * R)));
+    const size_t smem = smem_bytes(R, a.nstage, a.has_rest ? REST_STAGES : 0);
+    int per_sm = (int)std::min<size_t>(3, (227 * 1024) / (smem + 1024));
+    if (env_ctas > 0) per_sm = std::min<int>(env_ctas, (int)((227 * 1024) / (smem + 1024)));
     const int64_t n_tiles = tile_end - tile_begin;
     const int64_t cap = (int64_t)sm_count() * std::max(1, per_sm);
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
