@@ -5,21 +5,25 @@
 //
 //   * persistent grid (SMs x CTAs/SM); CTA c owns tiles c, c+grid, ... of the
 //     shared tiling (tiling_of: TILE = 256*R rows inside one row block);
-//   * warp 8 is the producer: one lane streams, per tile,
+//   * warp 8 is the producer.  One lane streams, per tile,
 //       - the tile's CSR remainder (col_ind and values of rows [lo, hi), in
-//         chunks of REST_CHUNK entries, 16-byte aligned windows) into a
-//         2-stage "rest" ring, then
-//       - every (tile, segment) slice -- TILE contiguous doubles of segment k --
-//         into an NSTAGE-deep "segment" ring,
-//     with cp.async.bulk (the 1-D TMA path, UBLKCP in SASS), completion through
-//     mbarrier transaction counts, L2 evict-first (everything it moves is read once);
-//   * warps 0-7 consume in the reference's order: remainder products (x gathered
-//     through L1/L2) written back in place in shared memory, per-row sequential
-//     sums, then per segment: wait for the slice, read the thread's R slots,
-//     multiply with x (issued ahead per group of XGROUP segments), add, release;
-//   * the producer runs up to NSTAGE slices + 2 remainder chunks ahead of the
-//     consumers, across tile boundaries, so each SM keeps well over 100 KB of
-//     matrix traffic in flight at a few instructions per 4 KB;
+//         chunks of REST_CHUNK entries, 16-byte aligned windows) into a 2-stage
+//         "rest" ring, then
+//       - for every segment k of the tile's block one stage of the main ring:
+//         the segment slice (TILE contiguous doubles) AND the x window the slice
+//         multiplies (x[lo+o_k, hi+o_k) clipped to the valid columns, widened to
+//         16-byte boundaries), plus a 16-byte descriptor (window shift, valid
+//         row range) written before the stage's mbarrier arrive,
+//     with cp.async.bulk (the 1-D TMA path, UBLKCP in SASS; segment and remainder
+//     traffic with an L2 evict-first hint, x with the default policy because its
+//     far offsets are re-read by other tiles from L2);
+//   * warps 0-7 consume in the reference's order from shared memory only:
+//     remainder products (x gathered through L1/L2, written back in place),
+//     per-row sequential sums, then per stage: seg * x, added in stored order,
+//     and the stage released -- a dozen instructions per segment per thread and
+//     no global-memory latency on the segment path;
+//   * the ring keeps NSTAGE (tile, segment) stages in flight per CTA, so each
+//     SM has ~200 KB of matrix + x traffic outstanding;
 //   * y is stored once per tile (streaming store); the optional fused per-tile
 //     sum of squares has the same fixed reduction order as spmv.cu, with one
 //     consumer barrier per tile (double-buffered warp partials).
@@ -37,8 +41,7 @@ namespace {
 constexpr int CONSUMER_WARPS = 8;
 constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
-constexpr int XGROUP = 8;
-constexpr int REST_CHUNK = 1024;  // entries per remainder stage (multiple of 4)
+constexpr int REST_CHUNK = 1024;         // entries per remainder stage (multiple of 4)
 constexpr int REST_STAGES = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -70,12 +73,18 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS) : "memory"); }
@@ -87,7 +96,7 @@ struct TmaArgs {
     const int32_t* rest_rp;
     const int32_t* rest_col;  // padded: readable up to a multiple of 4 entries past nnz_rest
     const double* rest_val;
-    const double* x;
+    const double* x;  // x_local
     double* y;
     const double* x_scale;
     double* tile_sumsq;
@@ -116,27 +125,46 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     return g;
 }
 
-struct Smem {
-    double* ring;      // nstage * TILE
-    int32_t* rcol;     // REST_STAGES * REST_CHUNK
-    double* rval;      // REST_STAGES * REST_CHUNK
-    double* wsum;      // 2 * CONSUMER_WARPS
-    uint64_t* full;    // nstage
-    uint64_t* empty;   // nstage
-    uint64_t* rfull;   // REST_STAGES
-    uint64_t* rempty;  // REST_STAGES
+// Stage descriptor: x for local row t (= i - lo) of the tile is xs[t + rel],
+// valid for t in [va, vb) (outside, the row does not touch this diagonal).
+struct __align__(16) Desc {
+    int rel, va, vb, pad;
 };
 
-// rest_stages is 0 for matrices without a remainder (no ring reserved: keeps 3 CTAs/SM)
+template <int R>
+struct Layout {
+    static constexpr int TILE = CONSUMERS * R;
+    static constexpr int XS = TILE + 4;  // x window (2 extra on each side for the 16-B widening)
+    static constexpr size_t STAGE_BYTES = sizeof(double) * (TILE + XS);
+};
+
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int rest_stages) {
-    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
+    const size_t stage = sizeof(double) * (size_t)(2 * CONSUMERS * R + 4);
+    return stage * nstage + sizeof(Desc) * nstage + sizeof(double) * (rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
            sizeof(int32_t) * rest_stages * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
 }
 
-__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int rest_stages) {
+struct Smem {
+    double* seg;   // nstage * TILE
+    double* xs;    // nstage * XS
+    Desc* desc;    // nstage
+    double* rval;  // rest_stages * REST_CHUNK
+    double* wsum;  // 2 * CONSUMER_WARPS
+    int32_t* rcol;
+    uint64_t* full;
+    uint64_t* empty;
+    uint64_t* rfull;
+    uint64_t* rempty;
+};
+
+template <int R>
+__device__ __forceinline__ Smem carve(unsigned char* base, int nstage, int rest_stages) {
+    using L = Layout<R>;
     Smem s;
-    s.ring = reinterpret_cast<double*>(base);
-    s.rval = s.ring + (size_t)nstage * CONSUMERS * R;
+    s.seg = reinterpret_cast<double*>(base);
+    s.xs = s.seg + (size_t)nstage * L::TILE;
+    s.desc = reinterpret_cast<Desc*>(s.xs + (size_t)nstage * L::XS);
+    s.rval = reinterpret_cast<double*>(s.desc + nstage);
     s.wsum = s.rval + rest_stages * REST_CHUNK;
     s.rcol = reinterpret_cast<int32_t*>(s.wsum + 2 * CONSUMER_WARPS);
     s.full = reinterpret_cast<uint64_t*>(s.rcol + rest_stages * REST_CHUNK);
@@ -148,10 +176,11 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
 
 template <int R, bool SCALE, bool NORM>
 __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
-    constexpr int TILE = CONSUMERS * R;
+    using L = Layout<R>;
+    constexpr int TILE = L::TILE;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const Smem S = carve(smem_raw, R, a.nstage, a.has_rest ? REST_STAGES : 0);
     const int NS = a.nstage;
+    const Smem S = carve<R>(smem_raw, NS, a.has_rest ? REST_STAGES : 0);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -172,6 +201,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
         const uint64_t policy = evict_first_policy();
+        const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
         uint32_t it = 0, rit = 0;
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R>(a, tile);
@@ -185,19 +215,45 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                         const int s = rit % REST_STAGES;
                         if (rit >= REST_STAGES) mbar_wait(&S.rempty[s], ((rit / REST_STAGES) - 1) & 1);
                         mbar_expect_tx(&S.rfull[s], (uint32_t)cnt * 12u);
-                        bulk_g2s(S.rcol + s * REST_CHUNK, a.rest_col + c, (uint32_t)cnt * 4u, &S.rfull[s], policy);
-                        bulk_g2s(S.rval + s * REST_CHUNK, a.rest_val + c, (uint32_t)cnt * 8u, &S.rfull[s], policy);
+                        bulk_g2s_hint(S.rcol + s * REST_CHUNK, a.rest_col + c, (uint32_t)cnt * 4u, &S.rfull[s],
+                                      policy);
+                        bulk_g2s_hint(S.rval + s * REST_CHUNK, a.rest_val + c, (uint32_t)cnt * 8u, &S.rfull[s],
+                                      policy);
                     }
                 }
             }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
-            const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
+            const uint32_t seg_bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
             for (int k = k0; k < k1; ++k, ++it, src += a.bl) {
                 const int s = it % NS;
                 if (it >= (uint32_t)NS) mbar_wait(&S.empty[s], ((it / NS) - 1) & 1);
-                mbar_expect_tx(&S.full[s], bytes);
-                bulk_g2s(S.ring + s * TILE, src, bytes, &S.full[s], policy);
+                // x window of this slice: x_local[lo+o, hi+o) clipped, widened to 16 B
+                const int64_t o = __ldg(a.dia_off + k);
+                const int64_t wa = max(g.lo + o, xlo_valid), wb = min(g.hi + o, xhi_valid);
+                uint32_t x_bytes = 0;
+                Desc d;
+                d.pad = 0;
+                if (wa < wb) {
+                    const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.x + wa) & ~uintptr_t(15);
+                    const uintptr_t p1 = (reinterpret_cast<uintptr_t>(a.x + wb) + 15) & ~uintptr_t(15);
+                    const int64_t A = (int64_t)(p0 - reinterpret_cast<uintptr_t>(a.x)) / 8;  // may be < 0
+                    x_bytes = (uint32_t)(p1 - p0);
+                    d.rel = (int)(g.lo + o - A);
+                    d.va = (int)(wa - (g.lo + o));
+                    d.vb = (int)(wb - (g.lo + o));
+                    S.desc[s] = d;
+                    mbar_expect_tx(&S.full[s], seg_bytes + x_bytes);
+                    bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
+                    bulk_g2s(S.xs + s * L::XS, reinterpret_cast<const void*>(p0), x_bytes, &S.full[s]);
+                } else {
+                    d.rel = 0;
+                    d.va = 0;
+                    d.vb = 0;
+                    S.desc[s] = d;
+                    mbar_expect_tx(&S.full[s], seg_bytes);
+                    bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
+                }
             }
         }
         return;
@@ -207,14 +263,15 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
     uint32_t it = 0, rit = 0, par = 0;
+    const int t0 = R * threadIdx.x;  // local row of this thread's first row
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R>(a, tile);
         if (g.lo >= g.hi) {
             if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
             continue;
         }
-        const int64_t i0 = g.lo + (int64_t)R * threadIdx.x;
-        const bool active = i0 < g.hi;
+        const int rows = (int)(g.hi - g.lo);
+        const int64_t i0 = g.lo + t0;
         double acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -226,7 +283,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                 int64_t kb[R], ke[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const bool ok = i0 + r < g.hi;
+                    const bool ok = t0 + r < rows;
                     kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
                     ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
                 }
@@ -257,72 +314,49 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             }
         }
 
-        // diagonal segments, stored order
-        const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
-        const int64_t glo = a.row0 + g.lo, ghi = a.row0 + g.hi;  // global rows [glo, ghi)
-        const double* xrow = a.x + i0;
-        for (int kg = k0; kg < k1; kg += XGROUP) {
-            double xv[XGROUP][R];
-#pragma unroll
-            for (int u = 0; u < XGROUP; ++u) {
-#pragma unroll
-                for (int r = 0; r < R; ++r) xv[u][r] = 0.0;
-                const int k = kg + u;
-                if (k < k1 && active) {
-                    const int64_t o = __ldg(a.dia_off + k);
-                    if (glo + o >= 0 && ghi - 1 + o < a.n_cols) {  // whole tile in range (uniform)
-#pragma unroll
-                        for (int r = 0; r < R; ++r)
-                            if (i0 + r < g.hi) xv[u][r] = __ldg(xrow + r + o);
-                    } else {
-#pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const int64_t j = a.row0 + i0 + r + o;
-                            if (j >= 0 && j < a.n_cols && i0 + r < g.hi) xv[u][r] = __ldg(xrow + r + o);
-                        }
-                    }
-                }
+        // diagonal segments, stored order, all operands in shared memory
+        const int nk = __ldg(a.dia_ptr + g.b + 1) - __ldg(a.dia_ptr + g.b);
+        for (int k = 0; k < nk; ++k) {
+            const int s = it % NS;
+            mbar_wait(&S.full[s], (it / NS) & 1);
+            const Desc d = S.desc[s];
+            const double* sv = S.seg + s * TILE + t0;
+            const double* xw = S.xs + s * L::XS + t0 + d.rel;
+            double v[R], xv[R];
+            if (R == 2) {
+                const double2 t = *reinterpret_cast<const double2*>(sv);
+                v[0] = t.x;
+                v[R - 1] = t.y;
+            } else {
+                v[0] = sv[0];
             }
 #pragma unroll
-            for (int u = 0; u < XGROUP; ++u) {
-                if (kg + u >= k1) break;
-                const int s = it % NS;
-                mbar_wait(&S.full[s], (it / NS) & 1);
-                const double* st = S.ring + s * TILE + R * threadIdx.x;
-                double v[R];
-                if (R == 2) {
-                    const double2 t = *reinterpret_cast<const double2*>(st);
-                    v[0] = t.x;
-                    v[R - 1] = t.y;
-                } else {
-                    v[0] = st[0];
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&S.empty[s]);
-                ++it;
+            for (int r = 0; r < R; ++r) xv[r] = (t0 + r >= d.va && t0 + r < d.vb) ? xw[r] : 0.0;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[s]);
+            ++it;
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    double xx = xv[u][r];
-                    if (SCALE) xx = __dmul_rn(xx, sc);
-                    acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
-                }
+            for (int r = 0; r < R; ++r) {
+                double xx = xv[r];
+                if (SCALE) xx = __dmul_rn(xx, sc);
+                acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
             }
         }
 
-        if (active) {
-            if (R == 2 && a.y_vec_ok && i0 + 1 < g.hi) {
+        if (t0 < rows) {
+            if (R == 2 && a.y_vec_ok && t0 + 1 < rows) {
                 __stcs(reinterpret_cast<double2*>(a.y + i0), make_double2(acc[0], acc[R - 1]));
             } else {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (i0 + r < g.hi) __stcs(a.y + i0 + r, acc[r]);
+                    if (t0 + r < rows) __stcs(a.y + i0 + r, acc[r]);
             }
         }
         if (NORM) {
             double s = 0.0;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (i0 + r < g.hi) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
+                if (t0 + r < rows) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
             double* ws = S.wsum + par * CONSUMER_WARPS;
@@ -344,7 +378,7 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM>;
     static size_t configured = 0;  // per instantiation
     if (configured < smem) {
-        const size_t cap = smem_bytes(R, 32, REST_STAGES);
+        const size_t cap = 227 * 1024;
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
         configured = cap;
     }
@@ -380,6 +414,7 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     if (m.bl % 2 != 0 || m.bl < CONSUMERS) return false;
     if (m.n_seg > 0 && ((uintptr_t)m.seg % 16) != 0) return false;
     if (m.nnz_rest > 0 && (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0)) return false;
+    if (((uintptr_t)x_local % 8) != 0) return false;
     const Tiling t = tiling_of(m);
     const int R = t.rows_per_thread;
     if (t.tiles_per_block <= 0 || t.tile_rows != (int64_t)CONSUMERS * R) return false;
@@ -404,17 +439,17 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
-    // ring depth: ~64 KB of segment slices, half that when a remainder ring is also needed
-    a.nstage = (a.has_rest ? 16 : 32) / R;
-    // tuning knobs for profiling sweeps (not needed in normal use)
-    static const int env_stage_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
+    // ring depth in KB of (segment + x) stages per CTA; 3 CTAs per SM
+    static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
-    if (env_stage_kb > 0) a.nstage = std::max(2, std::min(32, env_stage_kb / (2 * R)));
+    const int kb = env_kb > 0 ? env_kb : (a.has_rest ? 40 : 64);
+    const int stage_kb = 4 * R;  // seg + x for TILE = 256R rows
+    a.nstage = std::max(2, std::min(32, kb / stage_kb));
     const size_t smem = smem_bytes(R, a.nstage, a.has_rest ? REST_STAGES : 0);
-    int per_sm = (int)std::min<size_t>(3, (227 * 1024) / (smem + 1024));
-    if (env_ctas > 0) per_sm = std::min<int>(env_ctas, (int)((227 * 1024) / (smem + 1024)));
+    const int fit = (int)((227 * 1024) / (smem + 1024));
+    const int per_sm = std::max(1, std::min(env_ctas > 0 ? env_ctas : 3, fit));
     const int64_t n_tiles = tile_end - tile_begin;
-    const int64_t cap = (int64_t)sm_count() * std::max(1, per_sm);
+    const int64_t cap = (int64_t)sm_count() * per_sm;
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
     if (R == 2) launch_r<2>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
     else launch_r<1>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
