@@ -308,6 +308,8 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                         const int64_t p0 = max(kb[r], c), p1 = min(ke[r], c + REST_CHUNK);
                         for (int64_t p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], vs[p - c]);
                     }
+#pragma unroll
+                    for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));  // reads delivered
                     consumer_sync();
                     if (threadIdx.x == 0) mbar_arrive(&S.rempty[s]);
                 }
@@ -332,15 +334,21 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) xv[r] = (t0 + r >= d.va && t0 + r < d.vb) ? xw[r] : 0.0;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[s]);
-            ++it;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 double xx = xv[r];
                 if (SCALE) xx = __dmul_rn(xx, sc);
                 acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
             }
+            // Release the stage only once this thread's shared loads have delivered:
+            // the empty asm consumes acc (which depends on every value read), so the
+            // arrive cannot be issued while an LDS of this stage is still in flight,
+            // and __syncwarp orders the other lanes' reads before lane 0's arrive.
+#pragma unroll
+            for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[s]);
+            ++it;
         }
 
         if (t0 < rows) {
