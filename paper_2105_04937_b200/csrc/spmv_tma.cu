@@ -125,21 +125,30 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     return g;
 }
 
-// Stage descriptor: x for local row t (= i - lo) of the tile is xs[t + rel],
-// valid for t in [va, vb) (outside, the row does not touch this diagonal).
+// Offsets of a block within XSPAN columns of the cluster's first offset share one
+// x window (e.g. the {-1, 0, +1} groups of the 7- and 27-point stencils), loaded
+// with the cluster's first stage; at most CMAX segments per cluster.
+constexpr int XSPAN = 64;
+constexpr int CMAX = 4;
+
+// Stage descriptor: x for local row t (= i - lo) of the tile is
+// xs[stage it - back][t + rel], valid for t in [va, vb) (outside, the row does
+// not touch this diagonal).  release > 0 on a cluster's last segment: the
+// consumers then free that many stages (the whole cluster, windows included).
 struct __align__(16) Desc {
-    int rel, va, vb, pad;
+    int rel, va, vb;
+    short back, release;
 };
 
 template <int R>
 struct Layout {
     static constexpr int TILE = CONSUMERS * R;
-    static constexpr int XS = TILE + 4;  // x window (2 extra on each side for the 16-B widening)
+    static constexpr int XS = TILE + XSPAN + 4;  // cluster window (+2 each side for the 16-B widening)
     static constexpr size_t STAGE_BYTES = sizeof(double) * (TILE + XS);
 };
 
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int rest_stages) {
-    const size_t stage = sizeof(double) * (size_t)(2 * CONSUMERS * R + 4);
+    const size_t stage = sizeof(double) * (size_t)(2 * CONSUMERS * R + XSPAN + 4);
     return stage * nstage + sizeof(Desc) * nstage + sizeof(double) * (rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
            sizeof(int32_t) * rest_stages * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
 }
@@ -225,35 +234,49 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
             const uint32_t seg_bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
+            const int cmax = min(CMAX, NS - 1);
+            int kc = k0, ke = k0;  // current cluster [kc, ke)
+            int64_t A = 0;         // x_local index of the cluster window's first element
             for (int k = k0; k < k1; ++k, ++it, src += a.bl) {
                 const int s = it % NS;
                 if (it >= (uint32_t)NS) mbar_wait(&S.empty[s], ((it / NS) - 1) & 1);
-                // x window of this slice: x_local[lo+o, hi+o) clipped, widened to 16 B
                 const int64_t o = __ldg(a.dia_off + k);
-                const int64_t wa = max(g.lo + o, xlo_valid), wb = min(g.hi + o, xhi_valid);
                 uint32_t x_bytes = 0;
+                const void* x_src = nullptr;
+                if (k == ke) {
+                    // new cluster: extend while offsets stay within XSPAN of its first
+                    kc = k;
+                    ke = k + 1;
+                    while (ke < k1 && ke - kc < cmax && __ldg(a.dia_off + ke) - o <= XSPAN) ++ke;
+                    const int64_t o_last = __ldg(a.dia_off + ke - 1);
+                    // window x_local[lo+o, hi+o_last) clipped to the valid columns, widened to 16 B
+                    const int64_t wa = max(g.lo + o, xlo_valid), wb = min(g.hi + o_last, xhi_valid);
+                    if (wa < wb) {
+                        const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.x + wa) & ~uintptr_t(15);
+                        const uintptr_t p1 = (reinterpret_cast<uintptr_t>(a.x + wb) + 15) & ~uintptr_t(15);
+                        A = (int64_t)(p0 - reinterpret_cast<uintptr_t>(a.x)) / 8;  // may be < 0
+                        x_bytes = (uint32_t)(p1 - p0);
+                        x_src = reinterpret_cast<const void*>(p0);
+                    }
+                }
+                // this segment's own valid rows (a subset of the cluster window)
+                const int64_t va = max(g.lo + o, xlo_valid), vb = min(g.hi + o, xhi_valid);
                 Desc d;
-                d.pad = 0;
-                if (wa < wb) {
-                    const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.x + wa) & ~uintptr_t(15);
-                    const uintptr_t p1 = (reinterpret_cast<uintptr_t>(a.x + wb) + 15) & ~uintptr_t(15);
-                    const int64_t A = (int64_t)(p0 - reinterpret_cast<uintptr_t>(a.x)) / 8;  // may be < 0
-                    x_bytes = (uint32_t)(p1 - p0);
+                if (va < vb) {
                     d.rel = (int)(g.lo + o - A);
-                    d.va = (int)(wa - (g.lo + o));
-                    d.vb = (int)(wb - (g.lo + o));
-                    S.desc[s] = d;
-                    mbar_expect_tx(&S.full[s], seg_bytes + x_bytes);
-                    bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
-                    bulk_g2s(S.xs + s * L::XS, reinterpret_cast<const void*>(p0), x_bytes, &S.full[s]);
+                    d.va = (int)(va - (g.lo + o));
+                    d.vb = (int)(vb - (g.lo + o));
                 } else {
                     d.rel = 0;
                     d.va = 0;
                     d.vb = 0;
-                    S.desc[s] = d;
-                    mbar_expect_tx(&S.full[s], seg_bytes);
-                    bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
                 }
+                d.back = (short)(k - kc);
+                d.release = (short)(k == ke - 1 ? ke - kc : 0);
+                S.desc[s] = d;
+                mbar_expect_tx(&S.full[s], seg_bytes + x_bytes);
+                bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
+                if (x_bytes) bulk_g2s(S.xs + s * L::XS, x_src, x_bytes, &S.full[s]);
             }
         }
         return;
@@ -287,32 +310,57 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                     kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
                     ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
                 }
+                // Software pipeline over the tile's chunks: the x gathers of chunk c+1
+                // are in flight while the rows of chunk c are summed; one barrier per chunk.
+                constexpr int PER = REST_CHUNK / CONSUMERS;
                 const int64_t A = e_lo & ~int64_t(3), E = (e_hi + 3) & ~int64_t(3);
-                for (int64_t c = A; c < E; c += REST_CHUNK, ++rit) {
-                    const int s = rit % REST_STAGES;
-                    mbar_wait(&S.rfull[s], (rit / REST_STAGES) & 1);
-                    int32_t* cs = S.rcol + s * REST_CHUNK;
-                    double* vs = S.rval + s * REST_CHUNK;
-                    const int64_t q0 = max(c, e_lo), q1 = min(c + REST_CHUNK, e_hi);
-                    for (int64_t q = q0 + threadIdx.x; q < q1; q += CONSUMERS) {
-                        const int e = (int)(q - c);
-                        double xv = __ldg(a.x + ((int64_t)cs[e] - a.row0));
-                        if (SCALE) xv = __dmul_rn(xv, sc);
-                        vs[e] = __dmul_rn(vs[e], xv);
+                const int nch = (int)((E - A + REST_CHUNK - 1) / REST_CHUNK);
+                double xg[PER];
+                auto gather = [&](int ci) {  // wait for chunk ci, issue its x gathers
+                    const int64_t c = A + (int64_t)ci * REST_CHUNK;
+                    const uint32_t u = rit + ci;
+                    mbar_wait(&S.rfull[u % REST_STAGES], (u / REST_STAGES) & 1);
+                    const int32_t* cs = S.rcol + (u % REST_STAGES) * REST_CHUNK;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        const int64_t q = c + threadIdx.x + j * CONSUMERS;
+                        xg[j] = (q >= e_lo && q < e_hi) ? __ldg(a.x + ((int64_t)cs[q - c] - a.row0)) : 0.0;
+                    }
+                };
+                auto commit = [&](int ci) {  // products of chunk ci, in place
+                    const int64_t c = A + (int64_t)ci * REST_CHUNK;
+                    double* vs = S.rval + ((rit + ci) % REST_STAGES) * REST_CHUNK;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        const int64_t q = c + threadIdx.x + j * CONSUMERS;
+                        if (q >= e_lo && q < e_hi) {
+                            double xv = xg[j];
+                            if (SCALE) xv = __dmul_rn(xv, sc);
+                            vs[q - c] = __dmul_rn(vs[q - c], xv);
+                        }
                     }
                     // order these generic-proxy writes before the TMA refill of the stage
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    consumer_sync();
+                };
+                gather(0);
+                commit(0);
+                consumer_sync();
+                for (int ci = 0; ci < nch; ++ci) {
+                    if (ci + 1 < nch) gather(ci + 1);
+                    const int64_t c = A + (int64_t)ci * REST_CHUNK;
+                    const double* vs = S.rval + ((rit + ci) % REST_STAGES) * REST_CHUNK;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int64_t p0 = max(kb[r], c), p1 = min(ke[r], c + REST_CHUNK);
                         for (int64_t p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], vs[p - c]);
                     }
+                    if (ci + 1 < nch) commit(ci + 1);
 #pragma unroll
                     for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));  // reads delivered
                     consumer_sync();
-                    if (threadIdx.x == 0) mbar_arrive(&S.rempty[s]);
+                    if (threadIdx.x == 0) mbar_arrive(&S.rempty[(rit + ci) % REST_STAGES]);
                 }
+                rit += nch;
             }
         }
 
@@ -323,7 +371,8 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             mbar_wait(&S.full[s], (it / NS) & 1);
             const Desc d = S.desc[s];
             const double* sv = S.seg + s * TILE + t0;
-            const double* xw = S.xs + s * L::XS + t0 + d.rel;
+            const int xstage = (int)((it - (uint32_t)d.back) % (uint32_t)NS);
+            const double* xw = S.xs + xstage * L::XS + t0 + d.rel;
             double v[R], xv[R];
             if (R == 2) {
                 const double2 t = *reinterpret_cast<const double2*>(sv);
@@ -347,7 +396,8 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
             for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[s]);
+            if (lane == 0)
+                for (int q = 0; q < d.release; ++q) mbar_arrive(&S.empty[(it - q) % NS]);
             ++it;
         }
 
@@ -452,12 +502,17 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
     // 4 CTAs/SM (56 registers x 288 threads) with a ~41 KB ring each measured best
     // (c1 87%, c4 80% of HBM vs 76% / 71-74% with 3 CTAs and a 64 KB ring)
-    const int kb = env_kb > 0 ? env_kb : 44;
-    const int stage_kb = 4 * R;  // seg + x for TILE = 256R rows
-    a.nstage = std::max(2, std::min(32, kb / stage_kb));
+    // as many ring stages as fit next to 4 CTAs per SM (at most 8), unless overridden
+    const int want_ctas = env_ctas > 0 ? env_ctas : 4;
+    const size_t per_cta = (227 * 1024) / want_ctas - 1024;
+    const size_t fixed = smem_bytes(R, 0, a.has_rest ? REST_STAGES : 0);
+    const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
+    int ns = per_cta > fixed ? (int)((per_cta - fixed) / stage) : 2;
+    if (env_kb > 0) ns = (int)((size_t)env_kb * 1024 / stage);
+    a.nstage = std::max(2, std::min(env_kb > 0 ? 32 : 8, ns));
     const size_t smem = smem_bytes(R, a.nstage, a.has_rest ? REST_STAGES : 0);
     const int fit = (int)((227 * 1024) / (smem + 1024));
-    const int per_sm = std::max(1, std::min(env_ctas > 0 ? env_ctas : 4, fit));
+    const int per_sm = std::max(1, std::min(want_ctas, fit));
     const int64_t n_tiles = tile_end - tile_begin;
     const int64_t cap = (int64_t)sm_count() * per_sm;
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
