@@ -28,6 +28,8 @@
 //     order (bitwise order preserved, no warp-tree reordering);
 //   * y is written once (streaming store); optional fused epilogue emits the
 //     tile's sum of y_i^2 (power iteration) in a fixed reduction order.
+#include <cstdlib>
+
 #include "hdcg_internal.cuh"
 
 namespace hdcg {
@@ -249,6 +251,12 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
 
 void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                        const double* x_scale, double* tile_sumsq, cudaStream_t st) {
+    static const int env_policy = [] {  // HDCG_KERNEL_POLICY: profiling override of the default
+        const char* e = getenv("HDCG_KERNEL_POLICY");
+        if (e) g_kernel_policy = atoi(e);
+        return 0;
+    }();
+    (void)env_policy;
     const Tiling t = tiling_of(m);
     if (tile_begin < 0 || tile_end > t.n_tiles || tile_begin > tile_end)
         fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: tile range outside the matrix");

@@ -73,6 +73,16 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t evict_normal_policy() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                               uint64_t policy) {
     asm volatile(
@@ -106,6 +116,8 @@ struct TmaArgs {
     int nstage;
     int has_rest;
     int y_vec_ok;
+    int x_policy;  // L2 policy of the x windows: 0 default, 1 evict_last, 2 evict_normal
+    int cmax;      // max segments sharing one x window (1 = no sharing)
 };
 
 struct Geo {
@@ -210,6 +222,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
         const uint64_t policy = evict_first_policy();
+        const uint64_t xpolicy = a.x_policy == 1 ? evict_last_policy() : evict_normal_policy();
         const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
         uint32_t it = 0, rit = 0;
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
@@ -234,7 +247,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
             const uint32_t seg_bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
-            const int cmax = min(CMAX, NS - 1);
+            const int cmax = min(a.cmax, NS - 1);
             int kc = k0, ke = k0;  // current cluster [kc, ke)
             int64_t A = 0;         // x_local index of the cluster window's first element
             for (int k = k0; k < k1; ++k, ++it, src += a.bl) {
@@ -276,7 +289,10 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                 S.desc[s] = d;
                 mbar_expect_tx(&S.full[s], seg_bytes + x_bytes);
                 bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
-                if (x_bytes) bulk_g2s(S.xs + s * L::XS, x_src, x_bytes, &S.full[s]);
+                if (x_bytes) {
+                    if (a.x_policy == 0) bulk_g2s(S.xs + s * L::XS, x_src, x_bytes, &S.full[s]);
+                    else bulk_g2s_hint(S.xs + s * L::XS, x_src, x_bytes, &S.full[s], xpolicy);
+                }
             }
         }
         return;
@@ -497,6 +513,10 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
+    static const int env_xp = getenv("HDCG_TMA_X_POLICY") ? atoi(getenv("HDCG_TMA_X_POLICY")) : 0;
+    a.x_policy = env_xp;
+    static const int env_cmax = getenv("HDCG_TMA_CMAX") ? atoi(getenv("HDCG_TMA_CMAX")) : 0;
+    a.cmax = env_cmax > 0 ? std::min(env_cmax, CMAX) : CMAX;
     // ring depth in KB of (segment + x) stages per CTA; 3 CTAs per SM
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
