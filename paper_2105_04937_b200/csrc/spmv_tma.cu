@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         const uint64_t policy = evict_first_policy();
         const uint64_t xpolicy = a.x_policy == 1 ? evict_last_policy() : evict_normal_policy();
         const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
-        uint32_t it = 0, rit = 0;
+        uint32_t rit = 0;
+        int ps = 0;               // ring stage the next slice goes to
+        uint32_t pphase = 0;      // parity of that stage's current use
+        bool p_wrapped = false;   // every stage has been used once
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R>(a, tile);
             if (g.lo >= g.hi) continue;
@@ -250,9 +253,14 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             const int cmax = min(a.cmax, NS - 1);
             int kc = k0, ke = k0;  // current cluster [kc, ke)
             int64_t A = 0;         // x_local index of the cluster window's first element
-            for (int k = k0; k < k1; ++k, ++it, src += a.bl) {
-                const int s = it % NS;
-                if (it >= (uint32_t)NS) mbar_wait(&S.empty[s], ((it / NS) - 1) & 1);
+            for (int k = k0; k < k1; ++k, src += a.bl) {
+                const int s = ps;
+                if (p_wrapped) mbar_wait(&S.empty[s], pphase ^ 1u);  // previous use of this stage released
+                if (++ps == NS) {
+                    ps = 0;
+                    pphase ^= 1u;
+                    p_wrapped = true;
+                }
                 const int64_t o = __ldg(a.dia_off + k);
                 uint32_t x_bytes = 0;
                 const void* x_src = nullptr;
@@ -301,7 +309,9 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     // -------------------------------- consumers --------------------------------
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
-    uint32_t it = 0, rit = 0, par = 0;
+    uint32_t rit = 0, par = 0;
+    int cs_stage = 0;       // ring stage of the next slice to consume
+    uint32_t cs_phase = 0;  // parity of that stage's current use
     const int t0 = R * threadIdx.x;  // local row of this thread's first row
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R>(a, tile);
@@ -383,11 +393,12 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // diagonal segments, stored order, all operands in shared memory
         const int nk = __ldg(a.dia_ptr + g.b + 1) - __ldg(a.dia_ptr + g.b);
         for (int k = 0; k < nk; ++k) {
-            const int s = it % NS;
-            mbar_wait(&S.full[s], (it / NS) & 1);
+            const int s = cs_stage;
+            mbar_wait(&S.full[s], cs_phase);
             const Desc d = S.desc[s];
             const double* sv = S.seg + s * TILE + t0;
-            const int xstage = (int)((it - (uint32_t)d.back) % (uint32_t)NS);
+            int xstage = s - d.back;
+            if (xstage < 0) xstage += NS;
             const double* xw = S.xs + xstage * L::XS + t0 + d.rel;
             double v[R], xv[R];
             if (R == 2) {
@@ -412,9 +423,17 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
             for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
             __syncwarp();
-            if (lane == 0)
-                for (int q = 0; q < d.release; ++q) mbar_arrive(&S.empty[(it - q) % NS]);
-            ++it;
+            if (lane == 0) {
+                int q = s;
+                for (int c = 0; c < d.release; ++c) {  // the cluster's stages, newest first
+                    mbar_arrive(&S.empty[q]);
+                    q = q == 0 ? NS - 1 : q - 1;
+                }
+            }
+            if (++cs_stage == NS) {
+                cs_stage = 0;
+                cs_phase ^= 1u;
+            }
         }
 
         if (t0 < rows) {
