@@ -68,6 +68,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Consumer-side wait: the thread may be suspended up to `ns` nanoseconds per
+// try instead of spinning, leaving issue slots to the producer warp.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -118,6 +131,7 @@ struct TmaArgs {
     int y_vec_ok;
     int x_policy;  // L2 policy of the x windows: 0 default, 1 evict_last, 2 evict_normal
     int cmax;      // max segments sharing one x window (1 = no sharing)
+    int suspend_ns;  // consumer wait suspend hint (0: plain spin)
 };
 
 struct Geo {
@@ -394,7 +408,8 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         const int nk = __ldg(a.dia_ptr + g.b + 1) - __ldg(a.dia_ptr + g.b);
         for (int k = 0; k < nk; ++k) {
             const int s = cs_stage;
-            mbar_wait(&S.full[s], cs_phase);
+            if (a.suspend_ns > 0) mbar_wait_sleep(&S.full[s], cs_phase, (uint32_t)a.suspend_ns);
+            else mbar_wait(&S.full[s], cs_phase);
             const Desc d = S.desc[s];
             const double* sv = S.seg + s * TILE + t0;
             int xstage = s - d.back;
@@ -536,6 +551,8 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.x_policy = env_xp;
     static const int env_cmax = getenv("HDCG_TMA_CMAX") ? atoi(getenv("HDCG_TMA_CMAX")) : 0;
     a.cmax = env_cmax > 0 ? std::min(env_cmax, CMAX) : CMAX;
+    static const int env_susp = getenv("HDCG_TMA_SUSPEND_NS") ? atoi(getenv("HDCG_TMA_SUSPEND_NS")) : 0;
+    a.suspend_ns = env_susp;
     // ring depth in KB of (segment + x) stages per CTA; 3 CTAs per SM
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
