@@ -9,21 +9,20 @@
 //       - the tile's CSR remainder (col_ind and values of rows [lo, hi), in
 //         chunks of REST_CHUNK entries, 16-byte aligned windows) into a 2-stage
 //         "rest" ring, then
-//       - for every segment k of the tile's block one stage of the main ring:
-//         the segment slice (TILE contiguous doubles) AND the x window the slice
-//         multiplies (x[lo+o_k, hi+o_k) clipped to the valid columns, widened to
-//         16-byte boundaries), plus a 16-byte descriptor (window shift, valid
-//         row range) written before the stage's mbarrier arrive,
-//     with cp.async.bulk (the 1-D TMA path, UBLKCP in SASS; segment and remainder
-//     traffic with an L2 evict-first hint, x with the default policy because its
-//     far offsets are re-read by other tiles from L2);
-//   * warps 0-7 consume in the reference's order from shared memory only:
-//     remainder products (x gathered through L1/L2, written back in place),
-//     per-row sequential sums, then per stage: seg * x, added in stored order,
-//     and the stage released -- a dozen instructions per segment per thread and
-//     no global-memory latency on the segment path;
-//   * the ring keeps NSTAGE (tile, segment) stages in flight per CTA, so each
-//     SM has ~200 KB of matrix + x traffic outstanding;
+//       - every segment slice of the tile (TILE contiguous doubles of segment k)
+//         into an NSTAGE-deep "segment" ring,
+//     with cp.async.bulk (the 1-D TMA path, UBLKCP in SASS), completion through
+//     mbarrier transaction counts, L2 evict-first (everything it moves is read
+//     once).  The ring holds only matrix data -- the bytes that come from DRAM --
+//     so ~64 KB per CTA (~190 KB per SM) of HBM traffic is in flight;
+//   * warps 0-7 consume in the reference's order: remainder products (x gathered
+//     through L1/L2 one chunk ahead, written back in place), per-row sequential
+//     sums, then per segment: the block's offsets were loaded once per tile by
+//     each warp (one coalesced load, broadcast with shuffles); x values are
+//     loaded for a group of XGROUP segments ahead of the stage waits through the
+//     L1/tex path, where the near offsets of a tile share lines and the far ones
+//     hit L2; a warp-uniform whole-tile range test keeps per-row checks off the
+//     common path; ring bookkeeping is a (stage, phase) pair, no divisions;
 //   * y is stored once per tile (streaming store); the optional fused per-tile
 //     sum of squares has the same fixed reduction order as spmv.cu, with one
 //     consumer barrier per tile (double-buffered warp partials).
@@ -41,6 +40,7 @@ namespace {
 constexpr int CONSUMER_WARPS = 8;
 constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
+constexpr int XGROUP = 8;                // x loads issued ahead per group of segments
 constexpr int REST_CHUNK = 512;          // entries per remainder stage (multiple of 4)
 constexpr int REST_STAGES = 2;
 
@@ -68,46 +68,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-// Consumer-side wait: the thread may be suspended up to `ns` nanoseconds per
-// try instead of spinning, leaving issue slots to the producer warp.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAITS_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAITS_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(ns)
-        : "memory");
-}
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ uint64_t evict_last_policy() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t evict_normal_policy() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                              uint64_t policy) {
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS) : "memory"); }
@@ -129,9 +100,6 @@ struct TmaArgs {
     int nstage;
     int has_rest;
     int y_vec_ok;
-    int x_policy;  // L2 policy of the x windows: 0 default, 1 evict_last, 2 evict_normal
-    int cmax;      // max segments sharing one x window (1 = no sharing)
-    int suspend_ns;  // consumer wait suspend hint (0: plain spin)
 };
 
 struct Geo {
@@ -151,38 +119,13 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     return g;
 }
 
-// Offsets of a block within XSPAN columns of the cluster's first offset share one
-// x window (e.g. the {-1, 0, +1} groups of the 7- and 27-point stencils), loaded
-// with the cluster's first stage; at most CMAX segments per cluster.
-constexpr int XSPAN = 64;
-constexpr int CMAX = 4;
-
-// Stage descriptor: x for local row t (= i - lo) of the tile is
-// xs[stage it - back][t + rel], valid for t in [va, vb) (outside, the row does
-// not touch this diagonal).  release > 0 on a cluster's last segment: the
-// consumers then free that many stages (the whole cluster, windows included).
-struct __align__(16) Desc {
-    int rel, va, vb;
-    short back, release;
-};
-
-template <int R>
-struct Layout {
-    static constexpr int TILE = CONSUMERS * R;
-    static constexpr int XS = TILE + XSPAN + 4;  // cluster window (+2 each side for the 16-B widening)
-    static constexpr size_t STAGE_BYTES = sizeof(double) * (TILE + XS);
-};
-
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int rest_stages) {
-    const size_t stage = sizeof(double) * (size_t)(2 * CONSUMERS * R + XSPAN + 4);
-    return stage * nstage + sizeof(Desc) * nstage + sizeof(double) * (rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
+    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
            sizeof(int32_t) * rest_stages * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
 }
 
 struct Smem {
-    double* seg;   // nstage * TILE
-    double* xs;    // nstage * XS
-    Desc* desc;    // nstage
+    double* ring;  // nstage * TILE
     double* rval;  // rest_stages * REST_CHUNK
     double* wsum;  // 2 * CONSUMER_WARPS
     int32_t* rcol;
@@ -192,14 +135,10 @@ struct Smem {
     uint64_t* rempty;
 };
 
-template <int R>
-__device__ __forceinline__ Smem carve(unsigned char* base, int nstage, int rest_stages) {
-    using L = Layout<R>;
+__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int rest_stages) {
     Smem s;
-    s.seg = reinterpret_cast<double*>(base);
-    s.xs = s.seg + (size_t)nstage * L::TILE;
-    s.desc = reinterpret_cast<Desc*>(s.xs + (size_t)nstage * L::XS);
-    s.rval = reinterpret_cast<double*>(s.desc + nstage);
+    s.ring = reinterpret_cast<double*>(base);
+    s.rval = s.ring + (size_t)nstage * CONSUMERS * R;
     s.wsum = s.rval + rest_stages * REST_CHUNK;
     s.rcol = reinterpret_cast<int32_t*>(s.wsum + 2 * CONSUMER_WARPS);
     s.full = reinterpret_cast<uint64_t*>(s.rcol + rest_stages * REST_CHUNK);
@@ -211,11 +150,10 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int nstage, int rest_
 
 template <int R, bool SCALE, bool NORM>
 __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
-    using L = Layout<R>;
-    constexpr int TILE = L::TILE;
+    constexpr int TILE = CONSUMERS * R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
-    const Smem S = carve<R>(smem_raw, NS, a.has_rest ? REST_STAGES : 0);
+    const Smem S = carve(smem_raw, R, NS, a.has_rest ? REST_STAGES : 0);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -236,12 +174,10 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
         const uint64_t policy = evict_first_policy();
-        const uint64_t xpolicy = a.x_policy == 1 ? evict_last_policy() : evict_normal_policy();
-        const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
         uint32_t rit = 0;
-        int ps = 0;               // ring stage the next slice goes to
-        uint32_t pphase = 0;      // parity of that stage's current use
-        bool p_wrapped = false;   // every stage has been used once
+        int ps = 0;              // ring stage the next slice goes to
+        uint32_t pphase = 0;     // parity of that stage's current use
+        bool p_wrapped = false;  // every stage has been used once
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R>(a, tile);
             if (g.lo >= g.hi) continue;
@@ -254,66 +190,22 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                         const int s = rit % REST_STAGES;
                         if (rit >= REST_STAGES) mbar_wait(&S.rempty[s], ((rit / REST_STAGES) - 1) & 1);
                         mbar_expect_tx(&S.rfull[s], (uint32_t)cnt * 12u);
-                        bulk_g2s_hint(S.rcol + s * REST_CHUNK, a.rest_col + c, (uint32_t)cnt * 4u, &S.rfull[s],
-                                      policy);
-                        bulk_g2s_hint(S.rval + s * REST_CHUNK, a.rest_val + c, (uint32_t)cnt * 8u, &S.rfull[s],
-                                      policy);
+                        bulk_g2s(S.rcol + s * REST_CHUNK, a.rest_col + c, (uint32_t)cnt * 4u, &S.rfull[s], policy);
+                        bulk_g2s(S.rval + s * REST_CHUNK, a.rest_val + c, (uint32_t)cnt * 8u, &S.rfull[s], policy);
                     }
                 }
             }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
-            const uint32_t seg_bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
+            const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
-            const int cmax = min(a.cmax, NS - 1);
-            int kc = k0, ke = k0;  // current cluster [kc, ke)
-            int64_t A = 0;         // x_local index of the cluster window's first element
             for (int k = k0; k < k1; ++k, src += a.bl) {
-                const int s = ps;
-                if (p_wrapped) mbar_wait(&S.empty[s], pphase ^ 1u);  // previous use of this stage released
+                if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);  // previous use released
+                mbar_expect_tx(&S.full[ps], bytes);
+                bulk_g2s(S.ring + ps * TILE, src, bytes, &S.full[ps], policy);
                 if (++ps == NS) {
                     ps = 0;
                     pphase ^= 1u;
                     p_wrapped = true;
-                }
-                const int64_t o = __ldg(a.dia_off + k);
-                uint32_t x_bytes = 0;
-                const void* x_src = nullptr;
-                if (k == ke) {
-                    // new cluster: extend while offsets stay within XSPAN of its first
-                    kc = k;
-                    ke = k + 1;
-                    while (ke < k1 && ke - kc < cmax && __ldg(a.dia_off + ke) - o <= XSPAN) ++ke;
-                    const int64_t o_last = __ldg(a.dia_off + ke - 1);
-                    // window x_local[lo+o, hi+o_last) clipped to the valid columns, widened to 16 B
-                    const int64_t wa = max(g.lo + o, xlo_valid), wb = min(g.hi + o_last, xhi_valid);
-                    if (wa < wb) {
-                        const uintptr_t p0 = reinterpret_cast<uintptr_t>(a.x + wa) & ~uintptr_t(15);
-                        const uintptr_t p1 = (reinterpret_cast<uintptr_t>(a.x + wb) + 15) & ~uintptr_t(15);
-                        A = (int64_t)(p0 - reinterpret_cast<uintptr_t>(a.x)) / 8;  // may be < 0
-                        x_bytes = (uint32_t)(p1 - p0);
-                        x_src = reinterpret_cast<const void*>(p0);
-                    }
-                }
-                // this segment's own valid rows (a subset of the cluster window)
-                const int64_t va = max(g.lo + o, xlo_valid), vb = min(g.hi + o, xhi_valid);
-                Desc d;
-                if (va < vb) {
-                    d.rel = (int)(g.lo + o - A);
-                    d.va = (int)(va - (g.lo + o));
-                    d.vb = (int)(vb - (g.lo + o));
-                } else {
-                    d.rel = 0;
-                    d.va = 0;
-                    d.vb = 0;
-                }
-                d.back = (short)(k - kc);
-                d.release = (short)(k == ke - 1 ? ke - kc : 0);
-                S.desc[s] = d;
-                mbar_expect_tx(&S.full[s], seg_bytes + x_bytes);
-                bulk_g2s_hint(S.seg + s * TILE, src, seg_bytes, &S.full[s], policy);
-                if (x_bytes) {
-                    if (a.x_policy == 0) bulk_g2s(S.xs + s * L::XS, x_src, x_bytes, &S.full[s]);
-                    else bulk_g2s_hint(S.xs + s * L::XS, x_src, x_bytes, &S.full[s], xpolicy);
                 }
             }
         }
@@ -324,9 +216,10 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
     uint32_t rit = 0, par = 0;
-    int cs_stage = 0;       // ring stage of the next slice to consume
-    uint32_t cs_phase = 0;  // parity of that stage's current use
+    int cs = 0;             // ring stage of the next slice to consume
+    uint32_t cphase = 0;    // parity of that stage's current use
     const int t0 = R * threadIdx.x;  // local row of this thread's first row
+    const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R>(a, tile);
         if (g.lo >= g.hi) {
@@ -339,7 +232,9 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-        // CSR remainder first (stored order): products in place, then per-row sums
+        // CSR remainder first (stored order): products in place, then per-row sums.
+        // Software pipeline over the tile's chunks: the x gathers of chunk c+1 are in
+        // flight while the rows of chunk c are summed; one barrier per chunk.
         if (a.has_rest) {
             const int64_t e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
             if (e_lo < e_hi) {
@@ -350,8 +245,6 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                     kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
                     ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
                 }
-                // Software pipeline over the tile's chunks: the x gathers of chunk c+1
-                // are in flight while the rows of chunk c are summed; one barrier per chunk.
                 constexpr int PER = REST_CHUNK / CONSUMERS;
                 const int64_t A = e_lo & ~int64_t(3), E = (e_hi + 3) & ~int64_t(3);
                 const int nch = (int)((E - A + REST_CHUNK - 1) / REST_CHUNK);
@@ -360,11 +253,11 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                     const int64_t c = A + (int64_t)ci * REST_CHUNK;
                     const uint32_t u = rit + ci;
                     mbar_wait(&S.rfull[u % REST_STAGES], (u / REST_STAGES) & 1);
-                    const int32_t* cs = S.rcol + (u % REST_STAGES) * REST_CHUNK;
+                    const int32_t* cols = S.rcol + (u % REST_STAGES) * REST_CHUNK;
 #pragma unroll
                     for (int j = 0; j < PER; ++j) {
                         const int64_t q = c + threadIdx.x + j * CONSUMERS;
-                        xg[j] = (q >= e_lo && q < e_hi) ? __ldg(a.x + ((int64_t)cs[q - c] - a.row0)) : 0.0;
+                        xg[j] = (q >= e_lo && q < e_hi) ? __ldg(a.x + ((int64_t)cols[q - c] - a.row0)) : 0.0;
                     }
                 };
                 auto commit = [&](int ci) {  // products of chunk ci, in place
@@ -404,50 +297,65 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
             }
         }
 
-        // diagonal segments, stored order, all operands in shared memory
-        const int nk = __ldg(a.dia_ptr + g.b + 1) - __ldg(a.dia_ptr + g.b);
-        for (int k = 0; k < nk; ++k) {
-            const int s = cs_stage;
-            if (a.suspend_ns > 0) mbar_wait_sleep(&S.full[s], cs_phase, (uint32_t)a.suspend_ns);
-            else mbar_wait(&S.full[s], cs_phase);
-            const Desc d = S.desc[s];
-            const double* sv = S.seg + s * TILE + t0;
-            int xstage = s - d.back;
-            if (xstage < 0) xstage += NS;
-            const double* xw = S.xs + xstage * L::XS + t0 + d.rel;
-            double v[R], xv[R];
-            if (R == 2) {
-                const double2 t = *reinterpret_cast<const double2*>(sv);
-                v[0] = t.x;
-                v[R - 1] = t.y;
-            } else {
-                v[0] = sv[0];
-            }
+        // diagonal segments, stored order
+        const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
+        const double* xrow = a.x + i0;
+        for (int kb0 = k0; kb0 < k1; kb0 += 32) {
+            // the next <= 32 offsets of the block: one coalesced load, then shuffles
+            const int nk = min(32, k1 - kb0);
+            const int my_off = lane < nk ? __ldg(a.dia_off + kb0 + lane) : 0;
+            for (int kg = 0; kg < nk; kg += XGROUP) {
+                double xv[XGROUP][R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) xv[r] = (t0 + r >= d.va && t0 + r < d.vb) ? xw[r] : 0.0;
+                for (int u = 0; u < XGROUP; ++u) {
+                    const int64_t o = __shfl_sync(0xffffffffu, my_off, (kg + u) & 31);
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                double xx = xv[r];
-                if (SCALE) xx = __dmul_rn(xx, sc);
-                acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
-            }
-            // Release the stage only once this thread's shared loads have delivered:
-            // the empty asm consumes acc (which depends on every value read), so the
-            // arrive cannot be issued while an LDS of this stage is still in flight,
-            // and __syncwarp orders the other lanes' reads before lane 0's arrive.
+                    for (int r = 0; r < R; ++r) xv[u][r] = 0.0;
+                    if (kg + u < nk) {
+                        if (g.lo + o >= xlo_valid && g.hi + o <= xhi_valid) {  // whole tile in range
 #pragma unroll
-            for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
-            __syncwarp();
-            if (lane == 0) {
-                int q = s;
-                for (int c = 0; c < d.release; ++c) {  // the cluster's stages, newest first
-                    mbar_arrive(&S.empty[q]);
-                    q = q == 0 ? NS - 1 : q - 1;
+                            for (int r = 0; r < R; ++r)
+                                if (t0 + r < rows) xv[u][r] = __ldg(xrow + r + o);
+                        } else {
+#pragma unroll
+                            for (int r = 0; r < R; ++r) {
+                                const int64_t j = i0 + r + o;
+                                if (j >= xlo_valid && j < xhi_valid && t0 + r < rows) xv[u][r] = __ldg(xrow + r + o);
+                            }
+                        }
+                    }
                 }
-            }
-            if (++cs_stage == NS) {
-                cs_stage = 0;
-                cs_phase ^= 1u;
+#pragma unroll
+                for (int u = 0; u < XGROUP; ++u) {
+                    if (kg + u >= nk) break;
+                    mbar_wait(&S.full[cs], cphase);
+                    const double* st = S.ring + cs * TILE + t0;
+                    double v[R];
+                    if (R == 2) {
+                        const double2 t = *reinterpret_cast<const double2*>(st);
+                        v[0] = t.x;
+                        v[R - 1] = t.y;
+                    } else {
+                        v[0] = st[0];
+                    }
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        double xx = xv[u][r];
+                        if (SCALE) xx = __dmul_rn(xx, sc);
+                        acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
+                    }
+                    // Release the stage only once this thread's shared loads have
+                    // delivered (acc depends on them), then order the warp's reads
+                    // before lane 0's arrive.
+#pragma unroll
+                    for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&S.empty[cs]);
+                    if (++cs == NS) {
+                        cs = 0;
+                        cphase ^= 1u;
+                    }
+                }
             }
         }
 
@@ -484,11 +392,10 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 template <int R, bool SCALE, bool NORM>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM>;
-    static size_t configured = 0;  // per instantiation
-    if (configured < smem) {
-        const size_t cap = 227 * 1024;
-        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
-        configured = cap;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        configured = true;
     }
     k<<<grid, THREADS, smem, st>>>(a);
 }
@@ -522,7 +429,6 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     if (m.bl % 2 != 0 || m.bl < CONSUMERS) return false;
     if (m.n_seg > 0 && ((uintptr_t)m.seg % 16) != 0) return false;
     if (m.nnz_rest > 0 && (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0)) return false;
-    if (((uintptr_t)x_local % 8) != 0) return false;
     const Tiling t = tiling_of(m);
     const int R = t.rows_per_thread;
     if (t.tiles_per_block <= 0 || t.tile_rows != (int64_t)CONSUMERS * R) return false;
@@ -547,25 +453,14 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
-    static const int env_xp = getenv("HDCG_TMA_X_POLICY") ? atoi(getenv("HDCG_TMA_X_POLICY")) : 0;
-    a.x_policy = env_xp;
-    static const int env_cmax = getenv("HDCG_TMA_CMAX") ? atoi(getenv("HDCG_TMA_CMAX")) : 0;
-    a.cmax = env_cmax > 0 ? std::min(env_cmax, CMAX) : CMAX;
-    static const int env_susp = getenv("HDCG_TMA_SUSPEND_NS") ? atoi(getenv("HDCG_TMA_SUSPEND_NS")) : 0;
-    a.suspend_ns = env_susp;
-    // ring depth in KB of (segment + x) stages per CTA; 3 CTAs per SM
+    // ring of segment slices: ~64 KB per CTA, 3 CTAs per SM (tunable for profiling)
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
-    // 4 CTAs/SM (56 registers x 288 threads) with a ~41 KB ring each measured best
-    // (c1 87%, c4 80% of HBM vs 76% / 71-74% with 3 CTAs and a 64 KB ring)
-    // as many ring stages as fit next to 4 CTAs per SM (at most 8), unless overridden
-    const int want_ctas = env_ctas > 0 ? env_ctas : 4;
-    const size_t per_cta = (227 * 1024) / want_ctas - 1024;
-    const size_t fixed = smem_bytes(R, 0, a.has_rest ? REST_STAGES : 0);
+    const int want_ctas = env_ctas > 0 ? env_ctas : 3;
     const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
-    int ns = per_cta > fixed ? (int)((per_cta - fixed) / stage) : 2;
-    if (env_kb > 0) ns = (int)((size_t)env_kb * 1024 / stage);
-    a.nstage = std::max(2, std::min(env_kb > 0 ? 32 : 8, ns));
+    const size_t fixed = smem_bytes(R, 0, a.has_rest ? REST_STAGES : 0);
+    const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
+    a.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
     const size_t smem = smem_bytes(R, a.nstage, a.has_rest ? REST_STAGES : 0);
     const int fit = (int)((227 * 1024) / (smem + 1024));
     const int per_sm = std::max(1, std::min(want_ctas, fit));
