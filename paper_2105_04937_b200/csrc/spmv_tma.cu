@@ -5,19 +5,17 @@
 //
 //   * persistent grid (SMs x CTAs/SM); CTA c owns tiles c, c+grid, ... of the
 //     shared tiling (tiling_of: TILE = 256*R rows inside one row block);
-//   * warp 8 is the producer.  One lane streams, per tile,
-//       - the tile's CSR remainder (col_ind and values of rows [lo, hi), in
-//         chunks of REST_CHUNK entries, 16-byte aligned windows) into a 2-stage
-//         "rest" ring, then
-//       - every segment slice of the tile (TILE contiguous doubles of segment k)
-//         into an NSTAGE-deep "segment" ring,
-//     with cp.async.bulk (the 1-D TMA path, UBLKCP in SASS), completion through
-//     mbarrier transaction counts, L2 evict-first (everything it moves is read
-//     once).  The ring holds only matrix data -- the bytes that come from DRAM --
-//     so ~64 KB per CTA (~190 KB per SM) of HBM traffic is in flight;
-//   * warps 0-7 consume in the reference's order: remainder products (x gathered
-//     through L1/L2 one chunk ahead, written back in place), per-row sequential
-//     sums, then per segment: the block's offsets were loaded once per tile by
+//   * warp 8 is the producer.  One lane streams every segment slice of the tile
+//     (TILE contiguous doubles of segment k) into an NSTAGE-deep ring with
+//     cp.async.bulk (the 1-D TMA path, UBLKCP in SASS), completion through
+//     mbarrier transaction counts, L2 evict-first (segments are read once).  The
+//     ring holds only matrix data -- the bytes that come from DRAM -- so ~70 KB
+//     per CTA (~210 KB per SM) of HBM traffic is in flight;
+//   * warps 0-7 consume in the reference's order: first the CSR remainder, each
+//     warp for its own 32*R rows (their entries are contiguous: coalesced
+//     evict-first loads, 8 independent x gathers per lane in flight, products in
+//     a per-warp scratch, per-row sequential sums; warp-synchronous), then per
+//     segment: the block's offsets were loaded once per tile by
 //     each warp (one coalesced load, broadcast with shuffles); x values are
 //     loaded for a group of XGROUP segments ahead of the stage waits through the
 //     L1/tex path, where the near offsets of a tile share lines and the far ones
@@ -41,8 +39,7 @@ constexpr int CONSUMER_WARPS = 8;
 constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
 constexpr int XGROUP = 8;                // x loads issued ahead per group of segments
-constexpr int REST_CHUNK = 512;          // entries per remainder stage (multiple of 4)
-constexpr int REST_STAGES = 2;
+constexpr int WPASS = 256;               // remainder entries per warp pass (8 per lane)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -119,32 +116,28 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     return g;
 }
 
-__host__ __device__ inline size_t smem_bytes(int R, int nstage, int rest_stages) {
-    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + rest_stages * REST_CHUNK + 2 * CONSUMER_WARPS) +
-           sizeof(int32_t) * rest_stages * REST_CHUNK + sizeof(uint64_t) * (2 * nstage + 2 * REST_STAGES);
+// has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
+__host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest) {
+    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
+                             2 * CONSUMER_WARPS) +
+           sizeof(uint64_t) * (2 * nstage);
 }
 
 struct Smem {
-    double* ring;  // nstage * TILE
-    double* rval;  // rest_stages * REST_CHUNK
-    double* wsum;  // 2 * CONSUMER_WARPS
-    int32_t* rcol;
+    double* ring;     // nstage * TILE
+    double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
+    double* wsum;     // 2 * CONSUMER_WARPS
     uint64_t* full;
     uint64_t* empty;
-    uint64_t* rfull;
-    uint64_t* rempty;
 };
 
-__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int rest_stages) {
+__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int has_rest) {
     Smem s;
     s.ring = reinterpret_cast<double*>(base);
-    s.rval = s.ring + (size_t)nstage * CONSUMERS * R;
-    s.wsum = s.rval + rest_stages * REST_CHUNK;
-    s.rcol = reinterpret_cast<int32_t*>(s.wsum + 2 * CONSUMER_WARPS);
-    s.full = reinterpret_cast<uint64_t*>(s.rcol + rest_stages * REST_CHUNK);
+    s.scratch = s.ring + (size_t)nstage * CONSUMERS * R;
+    s.wsum = s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0);
+    s.full = reinterpret_cast<uint64_t*>(s.wsum + 2 * CONSUMER_WARPS);
     s.empty = s.full + nstage;
-    s.rfull = s.empty + nstage;
-    s.rempty = s.rfull + REST_STAGES;
     return s;
 }
 
@@ -153,7 +146,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
-    const Smem S = carve(smem_raw, R, NS, a.has_rest ? REST_STAGES : 0);
+    const Smem S = carve(smem_raw, R, NS, a.has_rest);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -161,10 +154,6 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&S.full[s], 1);
             mbar_init(&S.empty[s], CONSUMER_WARPS);
-        }
-        for (int s = 0; s < REST_STAGES; ++s) {
-            mbar_init(&S.rfull[s], 1);
-            mbar_init(&S.rempty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -174,27 +163,12 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // ------------------------------ producer ------------------------------
         if (lane != 0) return;
         const uint64_t policy = evict_first_policy();
-        uint32_t rit = 0;
         int ps = 0;              // ring stage the next slice goes to
         uint32_t pphase = 0;     // parity of that stage's current use
         bool p_wrapped = false;  // every stage has been used once
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R>(a, tile);
             if (g.lo >= g.hi) continue;
-            if (a.has_rest) {
-                const int64_t e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
-                if (e_lo < e_hi) {
-                    const int64_t A = e_lo & ~int64_t(3), E = (e_hi + 3) & ~int64_t(3);
-                    for (int64_t c = A; c < E; c += REST_CHUNK, ++rit) {
-                        const int cnt = (int)min((int64_t)REST_CHUNK, E - c);
-                        const int s = rit % REST_STAGES;
-                        if (rit >= REST_STAGES) mbar_wait(&S.rempty[s], ((rit / REST_STAGES) - 1) & 1);
-                        mbar_expect_tx(&S.rfull[s], (uint32_t)cnt * 12u);
-                        bulk_g2s(S.rcol + s * REST_CHUNK, a.rest_col + c, (uint32_t)cnt * 4u, &S.rfull[s], policy);
-                        bulk_g2s(S.rval + s * REST_CHUNK, a.rest_val + c, (uint32_t)cnt * 8u, &S.rfull[s], policy);
-                    }
-                }
-            }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
             const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
@@ -215,7 +189,7 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
     // -------------------------------- consumers --------------------------------
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
-    uint32_t rit = 0, par = 0;
+    uint32_t par = 0;
     int cs = 0;             // ring stage of the next slice to consume
     uint32_t cphase = 0;    // parity of that stage's current use
     const int t0 = R * threadIdx.x;  // local row of this thread's first row
@@ -232,11 +206,15 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-        // CSR remainder first (stored order): products in place, then per-row sums.
-        // Software pipeline over the tile's chunks: the x gathers of chunk c+1 are in
-        // flight while the rows of chunk c are summed; one barrier per chunk.
+        // CSR remainder first (stored order).  Each warp handles its own 32*R rows:
+        // the entries of those rows are contiguous, so lanes stream them coalesced
+        // (evict-first), gather x for WPASS/32 entries each (independent loads in
+        // flight), leave the products in the warp's scratch, and each lane then adds
+        // its rows' products sequentially.  Warp-synchronous: no block barrier.
         if (a.has_rest) {
-            const int64_t e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
+            const int64_t w_lo = min(g.lo + (int64_t)warp * 32 * R, g.hi);
+            const int64_t w_hi = min(w_lo + 32 * R, g.hi);
+            const int64_t e_lo = __ldg(a.rest_rp + w_lo), e_hi = __ldg(a.rest_rp + w_hi);
             if (e_lo < e_hi) {
                 int64_t kb[R], ke[R];
 #pragma unroll
@@ -245,55 +223,36 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                     kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
                     ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
                 }
-                constexpr int PER = REST_CHUNK / CONSUMERS;
-                const int64_t A = e_lo & ~int64_t(3), E = (e_hi + 3) & ~int64_t(3);
-                const int nch = (int)((E - A + REST_CHUNK - 1) / REST_CHUNK);
-                double xg[PER];
-                auto gather = [&](int ci) {  // wait for chunk ci, issue its x gathers
-                    const int64_t c = A + (int64_t)ci * REST_CHUNK;
-                    const uint32_t u = rit + ci;
-                    mbar_wait(&S.rfull[u % REST_STAGES], (u / REST_STAGES) & 1);
-                    const int32_t* cols = S.rcol + (u % REST_STAGES) * REST_CHUNK;
+                double* scratch = S.scratch + warp * WPASS;
+                constexpr int PER = WPASS / 32;
+                for (int64_t c = e_lo; c < e_hi; c += WPASS) {
+                    int32_t cl[PER];
+                    double vl[PER], xl[PER];
 #pragma unroll
                     for (int j = 0; j < PER; ++j) {
-                        const int64_t q = c + threadIdx.x + j * CONSUMERS;
-                        xg[j] = (q >= e_lo && q < e_hi) ? __ldg(a.x + ((int64_t)cols[q - c] - a.row0)) : 0.0;
+                        const int64_t q = c + lane + 32 * j;
+                        cl[j] = q < e_hi ? __ldcs(a.rest_col + q) : 0;
+                        vl[j] = q < e_hi ? __ldcs(a.rest_val + q) : 0.0;
                     }
-                };
-                auto commit = [&](int ci) {  // products of chunk ci, in place
-                    const int64_t c = A + (int64_t)ci * REST_CHUNK;
-                    double* vs = S.rval + ((rit + ci) % REST_STAGES) * REST_CHUNK;
 #pragma unroll
                     for (int j = 0; j < PER; ++j) {
-                        const int64_t q = c + threadIdx.x + j * CONSUMERS;
-                        if (q >= e_lo && q < e_hi) {
-                            double xv = xg[j];
-                            if (SCALE) xv = __dmul_rn(xv, sc);
-                            vs[q - c] = __dmul_rn(vs[q - c], xv);
-                        }
+                        const int64_t q = c + lane + 32 * j;
+                        xl[j] = q < e_hi ? __ldg(a.x + ((int64_t)cl[j] - a.row0)) : 0.0;
                     }
-                    // order these generic-proxy writes before the TMA refill of the stage
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                };
-                gather(0);
-                commit(0);
-                consumer_sync();
-                for (int ci = 0; ci < nch; ++ci) {
-                    if (ci + 1 < nch) gather(ci + 1);
-                    const int64_t c = A + (int64_t)ci * REST_CHUNK;
-                    const double* vs = S.rval + ((rit + ci) % REST_STAGES) * REST_CHUNK;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        double xv = xl[j];
+                        if (SCALE) xv = __dmul_rn(xv, sc);
+                        scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
+                    }
+                    __syncwarp();
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int64_t p0 = max(kb[r], c), p1 = min(ke[r], c + REST_CHUNK);
-                        for (int64_t p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], vs[p - c]);
+                        const int64_t p0 = max(kb[r], c), p1 = min(ke[r], c + WPASS);
+                        for (int64_t p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], scratch[p - c]);
                     }
-                    if (ci + 1 < nch) commit(ci + 1);
-#pragma unroll
-                    for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));  // reads delivered
-                    consumer_sync();
-                    if (threadIdx.x == 0) mbar_arrive(&S.rempty[(rit + ci) % REST_STAGES]);
+                    __syncwarp();
                 }
-                rit += nch;
             }
         }
 
@@ -458,10 +417,10 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
     const int want_ctas = env_ctas > 0 ? env_ctas : 3;
     const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
-    const size_t fixed = smem_bytes(R, 0, a.has_rest ? REST_STAGES : 0);
+    const size_t fixed = smem_bytes(R, 0, a.has_rest);
     const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
     a.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
-    const size_t smem = smem_bytes(R, a.nstage, a.has_rest ? REST_STAGES : 0);
+    const size_t smem = smem_bytes(R, a.nstage, a.has_rest);
     const int fit = (int)((227 * 1024) / (smem + 1024));
     const int per_sm = std::max(1, std::min(want_ctas, fit));
     const int64_t n_tiles = tile_end - tile_begin;
