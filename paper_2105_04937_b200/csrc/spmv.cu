@@ -126,21 +126,25 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
         const int k1 = __ldg(a.dia_ptr + b + 1);
         const int64_t gi = a.row0 + i0;
         const double* seg_base = a.seg + l;
-        for (int k = k0; k < k1; k += SEG_UNROLL) {
-            double v[SEG_UNROLL][R];
-            double xv[SEG_UNROLL][R];
+        constexpr int U = R == 4 ? 4 : SEG_UNROLL;
+        for (int k = k0; k < k1; k += U) {
+            double v[U][R];
+            double xv[U][R];
 #pragma unroll
-            for (int u = 0; u < SEG_UNROLL; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int kk = k + u;
 #pragma unroll
                 for (int r = 0; r < R; ++r) { v[u][r] = 0.0; xv[u][r] = 0.0; }
                 if (kk < k1) {
                     const int64_t o = __ldg(a.dia_off + kk);
                     const double* sp = seg_base + (int64_t)kk * a.bl;
-                    if (R == 2) {
-                        const double2 t = __ldcs(reinterpret_cast<const double2*>(sp));
-                        v[u][0] = t.x;
-                        v[u][R - 1] = t.y;
+                    if (R >= 2) {
+#pragma unroll
+                        for (int h = 0; h < R / 2; ++h) {
+                            const double2 t = __ldcs(reinterpret_cast<const double2*>(sp) + h);
+                            v[u][2 * h] = t.x;
+                            v[u][2 * h + 1] = t.y;
+                        }
                     } else {
                         v[u][0] = __ldcs(sp);
                     }
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
             // zero slots contribute +-0.0, an identity on an accumulator that
             // can never be -0.0 (it starts at +0.0), so masked rows add nothing.
 #pragma unroll
-            for (int u = 0; u < SEG_UNROLL; ++u) {
+            for (int u = 0; u < U; ++u) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     double xx = xv[u][r];
@@ -164,8 +168,10 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                 }
             }
         }
-        if (R == 2 && a.y_vec_ok && i0 + 1 < hi) {
-            __stcs(reinterpret_cast<double2*>(a.y + i0), make_double2(acc[0], acc[R - 1]));
+        if (R >= 2 && a.y_vec_ok && i0 + R - 1 < hi) {
+#pragma unroll
+            for (int h = 0; h < R / 2; ++h)
+                __stcs(reinterpret_cast<double2*>(a.y + i0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));
         } else {
 #pragma unroll
             for (int r = 0; r < R; ++r)
@@ -193,14 +199,17 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 
 // One tiling for both kernels (spmv_kernel and spmv_tma_kernel), so per-tile
 // partial sums and block-range alignment do not depend on which one runs:
-//   even bl >= 512     : 2 rows/thread, 512-row tiles, ceil(bl/512) tiles per block
+//   bl % 4 == 0, >= 1024: 4 rows/thread, 1024-row tiles, ceil(bl/1024) tiles per block
+//   other even bl >= 512 : 2 rows/thread, 512-row tiles
 //   even bl in [256,512): 1 row/thread, 256-row tiles, 2 tiles per block
 //   even bl < 256      : 2 rows/thread, 512/bl whole blocks per tile
 //   odd bl             : 1 row/thread, 256-row tiles (or 256/bl blocks per tile)
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
     const bool even = m.bl % 2 == 0;
-    t.rows_per_thread = (even && (m.bl >= 2 * SPMV_THREADS || m.bl < SPMV_THREADS)) ? 2 : 1;
+    if (m.bl % 4 == 0 && m.bl >= 4 * SPMV_THREADS) t.rows_per_thread = 4;
+    else if (even && (m.bl >= 2 * SPMV_THREADS || m.bl < SPMV_THREADS)) t.rows_per_thread = 2;
+    else t.rows_per_thread = 1;
     t.tile_rows = (int64_t)SPMV_THREADS * t.rows_per_thread;
     if (m.bl >= t.tile_rows) {
         t.tiles_per_block = ceil_div(m.bl, t.tile_rows);
@@ -288,7 +297,8 @@ void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_
     a.has_rest = m.nnz_rest > 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
     const bool scale = x_scale != nullptr, norm = tile_sumsq != nullptr;
-    if (t.rows_per_thread == 2) launch_r<2>(a, n_tiles, scale, norm, st);
+    if (t.rows_per_thread == 4) launch_r<4>(a, n_tiles, scale, norm, st);
+    else if (t.rows_per_thread == 2) launch_r<2>(a, n_tiles, scale, norm, st);
     else launch_r<1>(a, n_tiles, scale, norm, st);
     HDCG_LAUNCH_CHECK("spmv_kernel");
 }

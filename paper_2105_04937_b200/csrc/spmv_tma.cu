@@ -38,8 +38,8 @@ namespace {
 constexpr int CONSUMER_WARPS = 8;
 constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
-constexpr int XGROUP = 8;                // x loads issued ahead per group of segments
-constexpr int WPASS = 256;               // remainder entries per warp pass (8 per lane)
+constexpr int XGROUP_ROWS = 16;          // x values loaded ahead per thread (segments x rows)
+constexpr int WPASS = 128;               // remainder entries per warp pass (4 per lane)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -142,8 +142,9 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
 }
 
 template <int R, bool SCALE, bool NORM>
-__global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
+__global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
+    constexpr int XG = XGROUP_ROWS / R;  // x registers per thread stay at XGROUP_ROWS doubles
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
     const Smem S = carve(smem_raw, R, NS, a.has_rest);
@@ -214,9 +215,9 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         if (a.has_rest) {
             const int64_t w_lo = min(g.lo + (int64_t)warp * 32 * R, g.hi);
             const int64_t w_hi = min(w_lo + 32 * R, g.hi);
-            const int64_t e_lo = __ldg(a.rest_rp + w_lo), e_hi = __ldg(a.rest_rp + w_hi);
+            const int e_lo = __ldg(a.rest_rp + w_lo), e_hi = __ldg(a.rest_rp + w_hi);  // int32: nnz_rest < 2^31
             if (e_lo < e_hi) {
-                int64_t kb[R], ke[R];
+                int kb[R], ke[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const bool ok = t0 + r < rows;
@@ -225,18 +226,18 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                 }
                 double* scratch = S.scratch + warp * WPASS;
                 constexpr int PER = WPASS / 32;
-                for (int64_t c = e_lo; c < e_hi; c += WPASS) {
+                for (int c = e_lo; c < e_hi; c += WPASS) {
                     int32_t cl[PER];
                     double vl[PER], xl[PER];
 #pragma unroll
                     for (int j = 0; j < PER; ++j) {
-                        const int64_t q = c + lane + 32 * j;
+                        const int q = c + lane + 32 * j;
                         cl[j] = q < e_hi ? __ldcs(a.rest_col + q) : 0;
                         vl[j] = q < e_hi ? __ldcs(a.rest_val + q) : 0.0;
                     }
 #pragma unroll
                     for (int j = 0; j < PER; ++j) {
-                        const int64_t q = c + lane + 32 * j;
+                        const int q = c + lane + 32 * j;
                         xl[j] = q < e_hi ? __ldg(a.x + ((int64_t)cl[j] - a.row0)) : 0.0;
                     }
 #pragma unroll
@@ -248,8 +249,8 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
                     __syncwarp();
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int64_t p0 = max(kb[r], c), p1 = min(ke[r], c + WPASS);
-                        for (int64_t p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], scratch[p - c]);
+                        const int p0 = max(kb[r], c), p1 = min(ke[r], c + WPASS);
+                        for (int p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], scratch[p - c]);
                     }
                     __syncwarp();
                 }
@@ -259,68 +260,75 @@ __global__ void __launch_bounds__(THREADS) spmv_tma_kernel(const TmaArgs a) {
         // diagonal segments, stored order
         const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
         const double* xrow = a.x + i0;
+        const bool full = rows == TILE;  // warp-uniform: no per-row predicates needed
         for (int kb0 = k0; kb0 < k1; kb0 += 32) {
             // the next <= 32 offsets of the block: one coalesced load, then shuffles
             const int nk = min(32, k1 - kb0);
             const int my_off = lane < nk ? __ldg(a.dia_off + kb0 + lane) : 0;
-            for (int kg = 0; kg < nk; kg += XGROUP) {
-                double xv[XGROUP][R];
+            for (int kg = 0; kg < nk; kg += XG) {
+                const int ng = min(XG, nk - kg);  // warp-uniform
+                double xv[XG][R];
 #pragma unroll
-                for (int u = 0; u < XGROUP; ++u) {
+                for (int u = 0; u < XG; ++u) {
                     const int64_t o = __shfl_sync(0xffffffffu, my_off, (kg + u) & 31);
 #pragma unroll
                     for (int r = 0; r < R; ++r) xv[u][r] = 0.0;
-                    if (kg + u < nk) {
-                        if (g.lo + o >= xlo_valid && g.hi + o <= xhi_valid) {  // whole tile in range
+                    if (u < ng) {
+                        if (full && g.lo + o >= xlo_valid && g.hi + o <= xhi_valid) {  // common case
 #pragma unroll
-                            for (int r = 0; r < R; ++r)
-                                if (t0 + r < rows) xv[u][r] = __ldg(xrow + r + o);
+                            for (int r = 0; r < R; ++r) xv[u][r] = __ldg(xrow + r + o);
                         } else {
 #pragma unroll
                             for (int r = 0; r < R; ++r) {
                                 const int64_t j = i0 + r + o;
-                                if (j >= xlo_valid && j < xhi_valid && t0 + r < rows) xv[u][r] = __ldg(xrow + r + o);
+                                if (t0 + r < rows && j >= xlo_valid && j < xhi_valid) xv[u][r] = __ldg(xrow + r + o);
                             }
                         }
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < XGROUP; ++u) {
-                    if (kg + u >= nk) break;
-                    mbar_wait(&S.full[cs], cphase);
-                    const double* st = S.ring + cs * TILE + t0;
-                    double v[R];
-                    if (R == 2) {
-                        const double2 t = *reinterpret_cast<const double2*>(st);
-                        v[0] = t.x;
-                        v[R - 1] = t.y;
-                    } else {
-                        v[0] = st[0];
-                    }
+                for (int u = 0; u < XG; ++u) {
+                    if (u < ng) {
+                        mbar_wait(&S.full[cs], cphase);
+                        const double* st = S.ring + cs * TILE + t0;
+                        double v[R];
+                        if (R >= 2) {
 #pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        double xx = xv[u][r];
-                        if (SCALE) xx = __dmul_rn(xx, sc);
-                        acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
-                    }
-                    // Release the stage only once this thread's shared loads have
-                    // delivered (acc depends on them), then order the warp's reads
-                    // before lane 0's arrive.
+                            for (int h = 0; h < R / 2; ++h) {
+                                const double2 t = reinterpret_cast<const double2*>(st)[h];
+                                v[2 * h] = t.x;
+                                v[2 * h + 1] = t.y;
+                            }
+                        } else {
+                            v[0] = st[0];
+                        }
 #pragma unroll
-                    for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&S.empty[cs]);
-                    if (++cs == NS) {
-                        cs = 0;
-                        cphase ^= 1u;
+                        for (int r = 0; r < R; ++r) {
+                            double xx = xv[u][r];
+                            if (SCALE) xx = __dmul_rn(xx, sc);
+                            acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
+                        }
+                        // Release the stage only once this thread's shared loads have
+                        // delivered (acc depends on them), then order the warp's reads
+                        // before lane 0's arrive.
+#pragma unroll
+                        for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&S.empty[cs]);
+                        if (++cs == NS) {
+                            cs = 0;
+                            cphase ^= 1u;
+                        }
                     }
                 }
             }
         }
 
         if (t0 < rows) {
-            if (R == 2 && a.y_vec_ok && t0 + 1 < rows) {
-                __stcs(reinterpret_cast<double2*>(a.y + i0), make_double2(acc[0], acc[R - 1]));
+            if (R >= 2 && a.y_vec_ok && t0 + R - 1 < rows) {
+#pragma unroll
+                for (int h = 0; h < R / 2; ++h)
+                    __stcs(reinterpret_cast<double2*>(a.y + i0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));
             } else {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
@@ -426,7 +434,8 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     const int64_t n_tiles = tile_end - tile_begin;
     const int64_t cap = (int64_t)sm_count() * per_sm;
     const int grid = (int)(n_tiles < cap ? n_tiles : cap);
-    if (R == 2) launch_r<2>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
+    if (R == 4) launch_r<4>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
+    else if (R == 2) launch_r<2>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
     else launch_r<1>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
     HDCG_LAUNCH_CHECK("spmv_tma_kernel");
     return true;

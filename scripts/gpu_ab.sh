@@ -11,8 +11,7 @@ run() {  # label, workload, env...
     python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$label', '$w', d['value'], d['roofline']['frac'])" >> gpurun_out/ab.log
 }
 for w in c1 c4 c2 c3; do
-  run c3_default $w
-  run c4_52k $w HDCG_TMA_CTAS=4
-  run c2_100k $w HDCG_TMA_CTAS=2
+  run default $w
+  run ctas2 $w HDCG_TMA_CTAS=2
 done
 timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/ab.log
