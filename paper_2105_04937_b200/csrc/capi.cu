@@ -362,8 +362,10 @@ hdcg_status hdcg_upload_mhdc(int64_t n, int64_t bl, const int32_t* dia_ptr, int6
                                           cudaMemcpyHostToDevice, st));
             }
             int64_t slots = 0, dia_nnz = 0;
-            for (int64_t b = 0; b < m->n_blocks; ++b)
+            for (int64_t b = 0; b < m->n_blocks; ++b) {
                 slots += (int64_t)(dia_ptr[b + 1] - dia_ptr[b]) * std::min(bl, n - b * bl);
+                m->max_seg_per_block = std::max<int64_t>(m->max_seg_per_block, dia_ptr[b + 1] - dia_ptr[b]);
+            }
             for (int64_t k = 0; k < n_seg * bl; ++k) dia_nnz += segments[k] != 0.0;
             m->dia_slots = slots;
             m->nnz_input = dia_nnz + nnz_rest;
@@ -426,6 +428,7 @@ hdcg_status hdcg_upload_hdc(int64_t n, int64_t n_diag, const int32_t* offsets, c
             int64_t dia_nnz = 0;
             for (int64_t k = 0; k < m->n_seg * m->bl; ++k) dia_nnz += lanes[k] != 0.0;
             m->dia_slots = m->n_seg * n;
+            m->max_seg_per_block = m->n_seg;
             m->nnz_input = dia_nnz + nnz_rest;
             HDCG_CUDA(cudaStreamSynchronize(st));
         } catch (...) {

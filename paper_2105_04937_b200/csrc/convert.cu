@@ -656,10 +656,13 @@ static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selec
     HDCG_CUDA(cudaMemcpyAsync(dp.data(), m->dia_ptr, sizeof(int32_t) * (n_blocks + 1),
                               cudaMemcpyDeviceToHost, st));
     HDCG_CUDA(cudaStreamSynchronize(st));
-    int64_t slots = 0;
-    for (int64_t b = 0; b < n_blocks; ++b)
+    int64_t slots = 0, mx = 0;
+    for (int64_t b = 0; b < n_blocks; ++b) {
         slots += (int64_t)(dp[b + 1] - dp[b]) * std::min(bl, in.n_rows - b * bl);
+        mx = std::max<int64_t>(mx, dp[b + 1] - dp[b]);
+    }
     m->dia_slots = slots;
+    m->max_seg_per_block = mx;
 }
 
 static void check_slab(const CsrInput& in, int64_t bl) {

@@ -48,6 +48,7 @@ struct Matrix {
     int device = 0;
     int64_t n_rows = 0, n_cols = 0, row0 = 0, bl = 1, n_blocks = 0;
     int64_t n_seg = 0, nnz_rest = 0, nnz_input = 0, dia_slots = 0;
+    int64_t max_seg_per_block = 0;  // selects rows per thread (tiling_of)
     int32_t* dia_ptr = nullptr;
     int32_t* dia_off = nullptr;
     double* seg = nullptr;

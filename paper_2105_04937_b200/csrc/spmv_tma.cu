@@ -39,7 +39,7 @@ constexpr int CONSUMER_WARPS = 8;
 constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
 constexpr int XGROUP_ROWS = 16;          // x values loaded ahead per thread (segments x rows)
-constexpr int WPASS = 128;               // remainder entries per warp pass (4 per lane)
+constexpr int WPASS = 256;               // remainder scratch per warp (entries per pass <= this)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -225,8 +225,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                     ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
                 }
                 double* scratch = S.scratch + warp * WPASS;
-                constexpr int PER = WPASS / 32;
-                for (int c = e_lo; c < e_hi; c += WPASS) {
+                constexpr int PER = R == 4 ? 4 : 8;  // entries per lane per pass (x gathers in flight)
+                constexpr int PASS = 32 * PER;
+                for (int c = e_lo; c < e_hi; c += PASS) {
                     int32_t cl[PER];
                     double vl[PER], xl[PER];
 #pragma unroll
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                     __syncwarp();
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int p0 = max(kb[r], c), p1 = min(ke[r], c + WPASS);
+                        const int p0 = max(kb[r], c), p1 = min(ke[r], c + PASS);
                         for (int p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], scratch[p - c]);
                     }
                     __syncwarp();
