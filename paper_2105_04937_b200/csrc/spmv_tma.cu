@@ -96,6 +96,7 @@ struct TmaArgs {
     int tile_begin, tile_end;
     int nstage;
     int has_rest;
+    int init_y;  // remainder sums already in y (rest_kernel ran first)
     int y_vec_ok;
 };
 
@@ -139,6 +140,88 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
     s.full = reinterpret_cast<uint64_t*>(s.wsum + 2 * CONSUMER_WARPS);
     s.empty = s.full + nstage;
     return s;
+}
+
+// Remainder sums (stored order, onto +0.0 accumulators) of one warp's 32*R rows
+// of the tile [lo, hi): the rows' entries are contiguous, so lanes stream them
+// coalesced (evict-first), gather x for PER entries each (independent loads in
+// flight), leave the products in the warp's scratch, and each lane then adds its
+// rows' products sequentially.  Warp-synchronous.
+template <int R, bool SCALE>
+__device__ __forceinline__ void warp_rest(const int32_t* __restrict__ rest_rp, const int32_t* __restrict__ rest_col,
+                                          const double* __restrict__ rest_val, const double* __restrict__ x,
+                                          int64_t row0, double sc, int64_t lo, int64_t hi, int warp, int lane,
+                                          double* scratch, double (&acc)[R]) {
+    const int t0 = R * (warp * 32 + lane);
+    const int rows = (int)(hi - lo);
+    const int64_t i0 = lo + t0;
+    const int64_t w_lo = min(lo + (int64_t)warp * 32 * R, hi);
+    const int64_t w_hi = min(w_lo + 32 * R, hi);
+    const int e_lo = __ldg(rest_rp + w_lo), e_hi = __ldg(rest_rp + w_hi);  // int32: nnz_rest < 2^31
+    if (e_lo >= e_hi) return;
+    int kb[R], ke[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const bool ok = t0 + r < rows;
+        kb[r] = ok ? __ldg(rest_rp + i0 + r) : 0;
+        ke[r] = ok ? __ldg(rest_rp + i0 + r + 1) : 0;
+    }
+    constexpr int PER = R == 4 ? 4 : 8;  // entries per lane per pass (x gathers in flight)
+    constexpr int PASS = 32 * PER;
+    static_assert(PASS <= WPASS, "scratch too small");
+    for (int c = e_lo; c < e_hi; c += PASS) {
+        int32_t cl[PER];
+        double vl[PER], xl[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int q = c + lane + 32 * j;
+            cl[j] = q < e_hi ? __ldcs(rest_col + q) : 0;
+            vl[j] = q < e_hi ? __ldcs(rest_val + q) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int q = c + lane + 32 * j;
+            xl[j] = q < e_hi ? __ldg(x + ((int64_t)cl[j] - row0)) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            double xv = xl[j];
+            if (SCALE) xv = __dmul_rn(xv, sc);
+            scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int p0 = max(kb[r], c), p1 = min(ke[r], c + PASS);
+            for (int p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], scratch[p - c]);
+        }
+        __syncwarp();
+    }
+}
+
+// Remainder-heavy matrices: the remainder sums of every tile, written to y, by a
+// non-persistent high-occupancy kernel (one CTA of 8 warps per tile, no ring), so
+// far more x gathers are in flight than beside the segment ring.  spmv_tma_kernel
+// then starts each row from y -- the same operations in the same order.
+template <int R, bool SCALE>
+__global__ void __launch_bounds__(CONSUMERS) rest_kernel(const TmaArgs a) {
+    __shared__ double scratch[CONSUMER_WARPS * WPASS];
+    const int tile = a.tile_begin + blockIdx.x;
+    const Geo g = geo<R>(a, tile);
+    if (g.lo >= g.hi) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double sc = 1.0;
+    if (SCALE) sc = *a.x_scale;
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
+                        scratch + warp * WPASS, acc);
+    const int t0 = R * threadIdx.x;
+    const int rows = (int)(g.hi - g.lo);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (t0 + r < rows) a.y[g.lo + t0 + r] = acc[r];
 }
 
 template <int R, bool SCALE, bool NORM>
@@ -207,55 +290,14 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-        // CSR remainder first (stored order).  Each warp handles its own 32*R rows:
-        // the entries of those rows are contiguous, so lanes stream them coalesced
-        // (evict-first), gather x for WPASS/32 entries each (independent loads in
-        // flight), leave the products in the warp's scratch, and each lane then adds
-        // its rows' products sequentially.  Warp-synchronous: no block barrier.
-        if (a.has_rest) {
-            const int64_t w_lo = min(g.lo + (int64_t)warp * 32 * R, g.hi);
-            const int64_t w_hi = min(w_lo + 32 * R, g.hi);
-            const int e_lo = __ldg(a.rest_rp + w_lo), e_hi = __ldg(a.rest_rp + w_hi);  // int32: nnz_rest < 2^31
-            if (e_lo < e_hi) {
-                int kb[R], ke[R];
+        // CSR remainder first (stored order).  Either fused here (few remainder
+        // entries) or already summed into y by rest_kernel (remainder-heavy matrices).
+        if (a.init_y) {
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const bool ok = t0 + r < rows;
-                    kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
-                    ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
-                }
-                double* scratch = S.scratch + warp * WPASS;
-                constexpr int PER = R == 4 ? 4 : 8;  // entries per lane per pass (x gathers in flight)
-                constexpr int PASS = 32 * PER;
-                for (int c = e_lo; c < e_hi; c += PASS) {
-                    int32_t cl[PER];
-                    double vl[PER], xl[PER];
-#pragma unroll
-                    for (int j = 0; j < PER; ++j) {
-                        const int q = c + lane + 32 * j;
-                        cl[j] = q < e_hi ? __ldcs(a.rest_col + q) : 0;
-                        vl[j] = q < e_hi ? __ldcs(a.rest_val + q) : 0.0;
-                    }
-#pragma unroll
-                    for (int j = 0; j < PER; ++j) {
-                        const int q = c + lane + 32 * j;
-                        xl[j] = q < e_hi ? __ldg(a.x + ((int64_t)cl[j] - a.row0)) : 0.0;
-                    }
-#pragma unroll
-                    for (int j = 0; j < PER; ++j) {
-                        double xv = xl[j];
-                        if (SCALE) xv = __dmul_rn(xv, sc);
-                        scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
-                    }
-                    __syncwarp();
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int p0 = max(kb[r], c), p1 = min(ke[r], c + PASS);
-                        for (int p = p0; p < p1; ++p) acc[r] = __dadd_rn(acc[r], scratch[p - c]);
-                    }
-                    __syncwarp();
-                }
-            }
+            for (int r = 0; r < R; ++r) acc[r] = t0 + r < rows ? a.y[i0 + r] : 0.0;
+        } else if (a.has_rest) {
+            warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
+                                S.scratch + warp * WPASS, acc);
         }
 
         // diagonal segments, stored order
@@ -420,7 +462,21 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_begin = (int)tile_begin;
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
+    a.init_y = 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
+    // Remainder-heavy (>= 1 entry per 4 rows on average): sum it in rest_kernel first.
+    static const int env_split = getenv("HDCG_REST_SPLIT") ? atoi(getenv("HDCG_REST_SPLIT")) : -1;
+    const bool split = env_split >= 0 ? (env_split > 0 && a.has_rest) : (m.nnz_rest * 4 >= m.n_rows && a.has_rest);
+    if (split) {
+        const unsigned nt = (unsigned)(tile_end - tile_begin);
+        const bool sc = x_scale != nullptr;
+        if (R == 4) sc ? rest_kernel<4, true><<<nt, CONSUMERS, 0, st>>>(a) : rest_kernel<4, false><<<nt, CONSUMERS, 0, st>>>(a);
+        else if (R == 2) sc ? rest_kernel<2, true><<<nt, CONSUMERS, 0, st>>>(a) : rest_kernel<2, false><<<nt, CONSUMERS, 0, st>>>(a);
+        else sc ? rest_kernel<1, true><<<nt, CONSUMERS, 0, st>>>(a) : rest_kernel<1, false><<<nt, CONSUMERS, 0, st>>>(a);
+        HDCG_LAUNCH_CHECK("rest_kernel");
+        a.has_rest = 0;
+        a.init_y = 1;
+    }
     // ring of segment slices: ~64 KB per CTA, 3 CTAs per SM (tunable for profiling)
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;

@@ -555,3 +555,34 @@ def test_reference_acceptance_through_gpu_shim():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "all 8 criteria passed" in r.stdout
+
+
+def test_remainder_fused_and_split_paths(port):
+    """The TMA kernel sums a sparse remainder in-kernel (fused) and a heavy one in a
+    separate rest_kernel first (split); both must be bitwise equal to the oracle."""
+    rng = np.random.default_rng(17)
+    rp, col, val = synth.laplacian7(32, 32, 32)
+    n = 32 ** 3
+    i = np.repeat(np.arange(n), np.diff(rp))
+    for extra in (200, 20000):  # n/4 = 8192 separates the two paths
+        r = rng.integers(0, n, extra)
+        c = rng.integers(0, n, extra)
+        rows = np.concatenate([i, r])
+        cols = np.concatenate([col.astype(np.int64), c])
+        vals = np.concatenate([val, rng.uniform(-1, 1, extra)])
+        rp2, col2, val2 = synth.coo_to_csr(n, rows, cols, vals)
+        x = synth.x_vector(n, 3)
+        for bl in (1024, 4096, 512):
+            ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
+            m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
+            assert_mhdc_equal(m, ref, (extra, bl))
+            want = port.spmv_mhdc(ref, x)
+            assert H.spmv_mhdc(m, x).tobytes() == want.tobytes(), (extra, bl)
+            # power-iteration form (scaled x, fused norm) through the slab entry point
+            xd = torch.from_numpy(x).cuda()
+            yd = torch.empty(n, dtype=torch.float64, device="cuda")
+            tiles = torch.empty(m.info.n_tiles, dtype=torch.float64, device="cuda")
+            sc = torch.tensor([0.25], dtype=torch.float64, device="cuda")
+            H.spmv_slab(m, xd.data_ptr(), yd.data_ptr(), 0, m.n_blocks, sc.data_ptr(), tiles.data_ptr())
+            torch.cuda.synchronize()
+            assert yd.cpu().numpy().tobytes() == port.spmv_mhdc(ref, x * 0.25).tobytes(), (extra, bl)
