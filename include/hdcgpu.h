@@ -192,6 +192,16 @@ hdcg_status hdcg_set_kernel_policy(int policy);
  * as one call over all tiles. */
 hdcg_status hdcg_tree_sum(const double* vals, int64_t count, double* out, void* stream);
 
+/* ---- device memory benchmark -----------------------------------------------
+ * Replaces hdc::bench::membench(n, mode, cfg) (proj/include/hdc/bench.hpp:33-45,
+ * bench.cpp:68-110) on the device: c[i] += a[i]*b[i] (mode 0, direct, 32 B per
+ * element) or c[i] += a[i]*b[idx[i]] (mode 1, indirect, 36 B per element),
+ * one untimed loop then n_loops timed loops of n_ites calls, best per-call
+ * average; loop_times (host, n_loops entries) may be NULL.  Errors as the
+ * reference: INVALID_ARGUMENT for n < 1, n_loops < 1 or n_ites < 1. */
+hdcg_status hdcg_membench(int64_t n, int mode, int n_loops, int n_ites, double* best_time_s,
+                          double* bytes_per_s, double* loop_times);
+
 /* ---- synthetic inputs (bench / test support, device side) ----------------
  * The same counter-based generator as paper_2105_04937_b200/synth.py:
  *   u(seed, stream, i) = (splitmix64(key(seed, stream) + i) >> 11) * 2^-53

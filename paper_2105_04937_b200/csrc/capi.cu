@@ -538,6 +538,17 @@ hdcg_status hdcg_spmv_host(hdcg_matrix h, const double* x, double* y) {
     });
 }
 
+hdcg_status hdcg_membench(int64_t n, int mode, int n_loops, int n_ites, double* best_time_s,
+                          double* bytes_per_s, double* loop_times) {
+    return guard([&] {
+        if (!best_time_s || !bytes_per_s) fail(HDCG_ERR_INVALID_ARGUMENT, "membench: null output");
+        if (n_loops < 1 || n_ites < 1) fail(HDCG_ERR_INVALID_ARGUMENT, "timing: n_loops and n_ites must be >= 1");
+        if (n < 1) fail(HDCG_ERR_INVALID_ARGUMENT, "membench: n must be >= 1");
+        use_device();
+        membench(n, mode, n_loops, n_ites, best_time_s, bytes_per_s, loop_times);
+    });
+}
+
 hdcg_status hdcg_set_kernel_policy(int policy) {
     return guard([&] {
         if (policy < 0 || policy > 2) fail(HDCG_ERR_INVALID_ARGUMENT, "kernel policy must be 0, 1 or 2");

@@ -108,6 +108,9 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st);
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
+// device membench (membench.cu)
+void membench(int64_t n, int mode, int n_loops, int n_ites, double* best_s, double* bytes_per_s,
+              double* loop_times);
 // synchronous SpMV on host buffers, H2D / kernel / D2H overlapped chunk by chunk
 void spmv_host_pipelined(Matrix* m, const double* x_host, double* y_host);
 void tree_sum_launch(const double* vals, int64_t count, double* out, cudaStream_t st);

@@ -45,6 +45,7 @@ EXPORTS = (
     "hdcg_build_csr", "hdcg_upload_mhdc", "hdcg_upload_hdc", "hdcg_free", "hdcg_get_info",
     "hdcg_export", "hdcg_rates", "hdcg_census", "hdcg_spmv", "hdcg_spmv_host", "hdcg_spmv_slab",
     "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7", "hdcg_set_kernel_policy",
+    "hdcg_membench",
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
@@ -106,6 +107,7 @@ def lib():
         "hdcg_spmv_slab": [vp, vp, vp, i64, i64, vp, vp, vp],
         "hdcg_tree_sum": [vp, i64, vp, vp],
         "hdcg_set_kernel_policy": [C.c_int],
+        "hdcg_membench": [i64, C.c_int, C.c_int, C.c_int, C.POINTER(f64), C.POINTER(f64), vp],
         "hdcg_gen_uniform_pm1": [C.c_uint64, C.c_uint64, i64, i64, vp, vp],
         "hdcg_gen_laplacian7": [i64, i64, i64, i64, i64, vp, vp, vp, C.POINTER(i64), vp],
     }
@@ -452,6 +454,30 @@ def gen_laplacian7(nx, ny, nz, z0, z1, rp_ptr, col_ptr, val_ptr, stream=0):
 
 def init(device: int = 0):
     check(lib().hdcg_init(device))
+
+
+class Measurement(NamedTuple):
+    """hdc::bench::Measurement (proj/include/hdc/bench.hpp:18-23)."""
+    best_time_s: float
+    loop_times_s: list
+    bytes_per_s: float
+
+
+MEM_BYTES_DIRECT = 32.0    # bench.hpp:40
+MEM_BYTES_INDIRECT = 36.0  # bench.hpp:41
+
+
+def membench(n: int, mode: str = "direct", n_loops: int = 20, n_ites: int = 1000) -> Measurement:
+    """hdc::bench::membench on the device (bench.cpp:68-110): c[i] += a[i]*b[i]
+    (direct) or a[i]*b[idx[i]] (indirect); best per-call average of n_loops
+    loops of n_ites calls after one warm-up loop."""
+    modes = {"direct": 0, "indirect": 1}
+    if mode not in modes:
+        raise ValueError(f"unknown memory mode: {mode}")
+    best, bps = C.c_double(), C.c_double()
+    loops = np.zeros(max(n_loops, 1), np.float64)
+    check(lib().hdcg_membench(n, modes[mode], n_loops, n_ites, C.byref(best), C.byref(bps), _ptr(loops)))
+    return Measurement(best.value, loops.tolist(), bps.value)
 
 
 def set_kernel_policy(policy: int):

@@ -586,3 +586,21 @@ def test_remainder_fused_and_split_paths(port):
             H.spmv_slab(m, xd.data_ptr(), yd.data_ptr(), 0, m.n_blocks, sc.data_ptr(), tiles.data_ptr())
             torch.cuda.synchronize()
             assert yd.cpu().numpy().tobytes() == port.spmv_mhdc(ref, x * 0.25).tobytes(), (extra, bl)
+
+
+def test_device_membench_protocol():
+    """bench.cpp:68-110 on the device: byte accounting, loop record, result check,
+    argument errors (acceptance.cpp criterion 8 restated)."""
+    n = 1 << 20
+    d = H.membench(n, "direct", n_loops=3, n_ites=4)
+    assert len(d.loop_times_s) == 3 and d.best_time_s == min(d.loop_times_s)
+    assert d.bytes_per_s == H.MEM_BYTES_DIRECT * n / d.best_time_s
+    i = H.membench(n, "indirect", n_loops=2, n_ites=3)
+    assert i.bytes_per_s == H.MEM_BYTES_INDIRECT * n / i.best_time_s
+    big = H.membench(1 << 27, "direct", n_loops=3, n_ites=5)
+    assert big.bytes_per_s > 3e12  # a B200 streams > 3 TB/s
+    for bad in ((0, "direct", 1, 1), (8, "direct", 0, 1), (8, "direct", 1, 0)):
+        with pytest.raises(ValueError):
+            H.membench(*bad)
+    with pytest.raises(ValueError):
+        H.membench(8, "sideways")
