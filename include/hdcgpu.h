@@ -148,6 +148,17 @@ hdcg_status hdcg_census(int64_t n, int64_t nnz, const void* row_ptr, const int32
                         int64_t bl, unsigned flags, int64_t* block_ptr, int32_t* offsets,
                         int64_t* counts, int64_t* n_entries);
 
+/* (theta, bl) parameter sweep, the loop of `hdcmv analyze` (proj/tools/hdcmv.cpp:93-140):
+ * for every theta, rates(to_hdc(m, theta)) and, for every bl, rates(to_mhdc(m, theta, bl))
+ * (convert.cpp:173-196), computed from ONE device census per block width instead of
+ * building each format.  out (host) holds n_theta x (1 + n_bl) records of 4 doubles
+ * {alpha, beta, dia_slots, n_diags or n_segments}, record (t, 0) for HDC and
+ * (t, 1 + j) for M-HDC with bls[j]; alpha = beta = NaN where rates() would throw
+ * (no nonzeros).  Requires nnz < 2^31 and 1 <= n_theta <= 64. */
+hdcg_status hdcg_analyze(int64_t n, int64_t nnz, const void* row_ptr, const int32_t* col_ind,
+                         const double* values, const double* thetas, int n_theta, const int64_t* bls,
+                         int n_bl, unsigned flags, double* out);
+
 /* ---- SpMV ------------------------------------------------------------------
  * hdcg_spmv replaces hdc::spmv_mhdc / spmv_hdc / spmv_bhdc / spmv_csr /
  * spmv_dia / spmv_bdia (proj/include/hdc/kernels.hpp:31-49).  One kernel

@@ -538,6 +538,20 @@ hdcg_status hdcg_spmv_host(hdcg_matrix h, const double* x, double* y) {
     });
 }
 
+hdcg_status hdcg_analyze(int64_t n, int64_t nnz, const void* row_ptr, const int32_t* col_ind,
+                         const double* values, const double* thetas, int n_theta, const int64_t* bls,
+                         int n_bl, unsigned flags, double* out) {
+    return guard([&] {
+        if (!thetas || !out || (n_bl > 0 && !bls)) fail(HDCG_ERR_INVALID_ARGUMENT, "analyze: null argument");
+        use_device();
+        cudaStream_t st = nullptr;
+        Staged s(st);
+        stage_csr(s, n, n, 0, nnz, row_ptr, col_ind, values, flags);
+        if (nnz > 0 && !values) fail(HDCG_ERR_INVALID_ARGUMENT, "analyze: values are required");
+        analyze(s.in, thetas, n_theta, bls, n_bl, out, st);
+    });
+}
+
 hdcg_status hdcg_membench(int64_t n, int mode, int n_loops, int n_ites, double* best_time_s,
                           double* bytes_per_s, double* loop_times) {
     return guard([&] {

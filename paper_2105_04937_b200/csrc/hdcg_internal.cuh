@@ -108,6 +108,9 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st);
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
+// (theta, bl) sweep from one census per block width (analyze.cu)
+void analyze(const CsrInput& in, const double* thetas, int n_theta, const int64_t* bls, int n_bl, double* out,
+             cudaStream_t st);
 // device membench (membench.cu)
 void membench(int64_t n, int mode, int n_loops, int n_ites, double* best_s, double* bytes_per_s,
               double* loop_times);

@@ -45,7 +45,7 @@ EXPORTS = (
     "hdcg_build_csr", "hdcg_upload_mhdc", "hdcg_upload_hdc", "hdcg_free", "hdcg_get_info",
     "hdcg_export", "hdcg_rates", "hdcg_census", "hdcg_spmv", "hdcg_spmv_host", "hdcg_spmv_slab",
     "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7", "hdcg_set_kernel_policy",
-    "hdcg_membench",
+    "hdcg_membench", "hdcg_analyze",
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
@@ -108,6 +108,7 @@ def lib():
         "hdcg_tree_sum": [vp, i64, vp, vp],
         "hdcg_set_kernel_policy": [C.c_int],
         "hdcg_membench": [i64, C.c_int, C.c_int, C.c_int, C.POINTER(f64), C.POINTER(f64), vp],
+        "hdcg_analyze": [i64, i64, vp, vp, vp, vp, C.c_int, vp, C.c_int, u, vp],
         "hdcg_gen_uniform_pm1": [C.c_uint64, C.c_uint64, i64, i64, vp, vp],
         "hdcg_gen_laplacian7": [i64, i64, i64, i64, i64, vp, vp, vp, C.POINTER(i64), vp],
     }
@@ -454,6 +455,37 @@ def gen_laplacian7(nx, ny, nz, z0, z1, rp_ptr, col_ptr, val_ptr, stream=0):
 
 def init(device: int = 0):
     check(lib().hdcg_init(device))
+
+
+class AnalyzeRow(NamedTuple):
+    """One line of `hdcmv analyze` (proj/tools/hdcmv.cpp:105-133)."""
+    kernel: str      # "hdc" or "mhdc"
+    theta: float
+    bl: int          # 0 for hdc
+    n_diag: int      # HdcMatrix::dia().n_diags() / MHdcMatrix::n_segments()
+    alpha: float     # NaN where rates() throws (no nonzeros)
+    beta: float
+    dia_slots: int
+
+
+def analyze(m: CsrMatrix, thetas, bls) -> list:
+    """The (theta, bl) sweep of `hdcmv analyze` (hdcmv.cpp:93-140): for each theta
+    the HDC split, then the M-HDC split for each bl -- rates computed from one
+    device census per block width (no format is built)."""
+    thetas = np.ascontiguousarray(thetas, dtype=np.float64)
+    bls = np.ascontiguousarray(bls, dtype=np.int64)
+    nt, nb = thetas.size, bls.size
+    out = np.zeros(nt * (1 + nb) * 4, np.float64)
+    check(lib().hdcg_analyze(m.n, m.nnz, _ptr(m.row_ptr), _ptr(m.col_ind), _ptr(m.values), _ptr(thetas), nt,
+                             _ptr(bls), nb, m._flags(), _ptr(out)))
+    out = out.reshape(nt, 1 + nb, 4)
+    rows = []
+    for t in range(nt):
+        for j in range(1 + nb):
+            a, b, slots, nd = out[t, j]
+            rows.append(AnalyzeRow("hdc" if j == 0 else "mhdc", float(thetas[t]), 0 if j == 0 else int(bls[j - 1]),
+                                   int(nd), float(a), float(b), int(slots)))
+    return rows
 
 
 class Measurement(NamedTuple):

@@ -604,3 +604,36 @@ def test_device_membench_protocol():
             H.membench(*bad)
     with pytest.raises(ValueError):
         H.membench(8, "sideways")
+
+
+def test_analyze_sweep_matches_rates(port, golden):
+    """hdcg_analyze (one census per bl) == rates(to_hdc/to_mhdc(m, theta, bl)) of the
+    oracle for every grid point, incl. explicit zeros and matrices without nonzeros."""
+    thetas = [0.0, 0.3, 0.5, 0.6, 0.9, 1.0]
+    cases = [str(nm) for nm in golden["names"]][:30]
+    mats = [(golden[p + "/rp"], golden[p + "/col"], golden[p + "/val"]) for p in cases]
+    rp, col, val = synth.laplacian7(12, 10, 9)
+    val = val.copy()
+    val[::5] = 0.0  # explicit zeros: counted by the census, not by nnz(dia part)
+    mats.append((rp, col, val))
+    mats.append((np.zeros(4, np.int64), np.zeros(0, np.int32), np.zeros(0)))
+    for rp, col, val in mats:
+        n = len(rp) - 1
+        bls = [1, 3, 7, 64, max(1, n + 2)]
+        rows = H.analyze(csr(rp, col, val), thetas, bls)
+        it = iter(rows)
+        for th in thetas:
+            for j, bl in enumerate([0] + bls):
+                r = next(it)
+                m = port.to_hdc(rp, col, val, th) if j == 0 else port.to_mhdc(rp, col, val, th, bl)
+                assert r.n_diag == m.n_seg, (n, th, bl)
+                try:
+                    a, b, s = port.rates(m)
+                except ValueError:
+                    assert np.isnan(r.alpha) and np.isnan(r.beta)
+                    continue
+                assert (r.alpha, r.beta, r.dia_slots) == (a, b, s), (n, th, bl)
+    with pytest.raises(ValueError):
+        H.analyze(csr(*synth.example_matrix()), [1.5], [4])
+    with pytest.raises(ValueError):
+        H.analyze(csr(*synth.example_matrix()), [0.5], [0])
