@@ -108,9 +108,6 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st);
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
-// (theta, bl) sweep from one census per block width (analyze.cu)
-void analyze(const CsrInput& in, const double* thetas, int n_theta, const int64_t* bls, int n_bl, double* out,
-             cudaStream_t st);
 // device membench (membench.cu)
 void membench(int64_t n, int mode, int n_loops, int n_ites, double* best_s, double* bytes_per_s,
               double* loop_times);
@@ -134,6 +131,9 @@ void build_csr(const CsrInput& in, Matrix* out, cudaStream_t st);
 int64_t census(const CsrInput& in, int64_t bl, int64_t* block_ptr_host, int32_t* offsets_host,
                int64_t* counts_host, cudaStream_t st);
 void rates(const Matrix& m, double* alpha, double* beta, int64_t* slots, cudaStream_t st);
+// (theta, bl) sweep from one census per block width (analyze.cu)
+void analyze(const CsrInput& in, const double* thetas, int n_theta, const int64_t* bls, int n_bl, double* out,
+             cudaStream_t st);
 // CUB exclusive scan of int64 (defined in convert.cu so only one TU includes CUB)
 cudaError_t cub_exclusive_sum_i64(void* tmp, size_t& bytes, const int64_t* in, int64_t* out,
                                   int64_t count, cudaStream_t st);
