@@ -203,25 +203,20 @@ __device__ __forceinline__ void warp_rest(const int32_t* __restrict__ rest_rp, c
 // non-persistent high-occupancy kernel (one CTA of 8 warps per tile, no ring), so
 // far more x gathers are in flight than beside the segment ring.  spmv_tma_kernel
 // then starts each row from y -- the same operations in the same order.
-template <int R, bool SCALE>
-__global__ void __launch_bounds__(CONSUMERS) rest_kernel(const TmaArgs a) {
+// It only writes y, so its row mapping is free: one row per lane (a warp's 32 rows
+// usually fit one pass of 8 gathers per lane), 256 rows per CTA, many CTAs per SM.
+template <bool SCALE>
+__global__ void __launch_bounds__(CONSUMERS) rest_kernel(const TmaArgs a, int64_t row_lo, int64_t row_hi) {
     __shared__ double scratch[CONSUMER_WARPS * WPASS];
-    const int tile = a.tile_begin + blockIdx.x;
-    const Geo g = geo<R>(a, tile);
-    if (g.lo >= g.hi) return;
+    const int64_t lo = row_lo + (int64_t)blockIdx.x * CONSUMERS;
+    const int64_t hi = min(lo + CONSUMERS, row_hi);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
-    double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
+    double acc[1] = {0.0};
+    warp_rest<1, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo, hi, warp, lane,
                         scratch + warp * WPASS, acc);
-    const int t0 = R * threadIdx.x;
-    const int rows = (int)(g.hi - g.lo);
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-        if (t0 + r < rows) a.y[g.lo + t0 + r] = acc[r];
+    if (lo + threadIdx.x < hi) a.y[lo + threadIdx.x] = acc[0];
 }
 
 template <int R, bool SCALE, bool NORM>
@@ -468,12 +463,17 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     static const int env_split = getenv("HDCG_REST_SPLIT") ? atoi(getenv("HDCG_REST_SPLIT")) : -1;
     const bool split = env_split >= 0 ? (env_split > 0 && a.has_rest) : (m.nnz_rest * 4 >= m.n_rows && a.has_rest);
     if (split) {
-        const unsigned nt = (unsigned)(tile_end - tile_begin);
-        const bool sc = x_scale != nullptr;
-        if (R == 4) sc ? rest_kernel<4, true><<<nt, CONSUMERS, 0, st>>>(a) : rest_kernel<4, false><<<nt, CONSUMERS, 0, st>>>(a);
-        else if (R == 2) sc ? rest_kernel<2, true><<<nt, CONSUMERS, 0, st>>>(a) : rest_kernel<2, false><<<nt, CONSUMERS, 0, st>>>(a);
-        else sc ? rest_kernel<1, true><<<nt, CONSUMERS, 0, st>>>(a) : rest_kernel<1, false><<<nt, CONSUMERS, 0, st>>>(a);
-        HDCG_LAUNCH_CHECK("rest_kernel");
+        // rows covered by the tile range (tiles are contiguous in rows)
+        int64_t r0, r1, dummy;
+        tile_rows(tile_begin, t.tiles_per_block, 0, t.tile_rows, m.bl, m.n_rows, &r0, &dummy);
+        tile_rows(tile_end - 1, t.tiles_per_block, 0, t.tile_rows, m.bl, m.n_rows, &dummy, &r1);
+        r0 = std::min(r0, m.n_rows);
+        if (r1 > r0) {
+            const unsigned nb = (unsigned)ceil_div(r1 - r0, CONSUMERS);
+            if (x_scale) rest_kernel<true><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
+            else rest_kernel<false><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
+            HDCG_LAUNCH_CHECK("rest_kernel");
+        }
         a.has_rest = 0;
         a.init_y = 1;
     }
