@@ -43,7 +43,8 @@ typedef enum {
     HDCG_ERR_OVERFLOW = 3,         /* std::overflow_error (index range exceeded) */
     HDCG_ERR_CUDA = 4,             /* CUDA runtime failure */
     HDCG_ERR_NO_DEVICE = 5,        /* no usable sm_100 device */
-    HDCG_ERR_OUT_OF_MEMORY = 6     /* std::bad_alloc */
+    HDCG_ERR_OUT_OF_MEMORY = 6,    /* std::bad_alloc */
+    HDCG_ERR_IO = 7                /* std::runtime_error from Matrix Market reading (io.cpp) */
 } hdcg_status;
 
 /* flags */
@@ -121,6 +122,15 @@ hdcg_status hdcg_upload_hdc(int64_t n, int64_t n_diag, const int32_t* offsets, c
                             const int32_t* rest_row_ptr, int64_t nnz_rest,
                             const int32_t* rest_col_ind, const double* rest_values,
                             unsigned flags, hdcg_matrix* out);
+
+/* Matrix Market file -> device-resident CSR handle (kind HDCG_KIND_CSR; the CSR
+ * arrays are what hdcg_export returns as the remainder).  Replaces
+ * hdc::io::read_matrix_market (proj/include/hdc/io.hpp:14-20, io.cpp:69-121) +
+ * CooMatrix normalisation (formats.cpp:19-43) + CsrMatrix::from_coo
+ * (formats.cpp:69-88): same accepted formats (coordinate real / integer /
+ * pattern; general / symmetric / skew-symmetric), same checks and messages
+ * (HDCG_ERR_IO), duplicates summed in file order, bit-identical arrays. */
+hdcg_status hdcg_read_matrix_market(const char* path, hdcg_matrix* out);
 
 hdcg_status hdcg_free(hdcg_matrix m);
 

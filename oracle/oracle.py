@@ -221,6 +221,7 @@ class Ref:
         L.refc_spmv.argtypes = [C.c_int, vp, C.c_int64, _f64p, _f64p, C.c_int64, C.c_int]
         L.refc_time_spmv.argtypes = [C.c_int, vp, C.c_int64, _f64p, _f64p, C.c_int64, C.c_int,
                                      C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.refc_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(vp)]
 
     def _check(self, rc):
         if rc != 0:
@@ -250,6 +251,19 @@ class Ref:
     def example_matrix(self):
         h = C.c_void_p()
         self._check(self.lib.refc_example_matrix(C.byref(h)))
+        n, nnz = C.c_int64(), C.c_int64()
+        self.lib.refc_csr_sizes(h, C.byref(n), C.byref(nnz))
+        rp = np.zeros(n.value + 1, np.int64)
+        col = np.zeros(nnz.value, np.int32)
+        val = np.zeros(nnz.value)
+        self.lib.refc_csr_export(h, rp, col, val)
+        self.lib.refc_csr_free(h)
+        return rp, col, val
+
+    def read_matrix_market(self, path):
+        """io.cpp:69-121 + CsrMatrix::from_coo -> (rp, col, val) host arrays."""
+        h = C.c_void_p()
+        self._check(self.lib.refc_read_matrix_market(os.fsencode(path), C.byref(h)))
         n, nnz = C.c_int64(), C.c_int64()
         self.lib.refc_csr_sizes(h, C.byref(n), C.byref(nnz))
         rp = np.zeros(n.value + 1, np.int64)

@@ -251,3 +251,20 @@ int refc_time_spmv(int kind, void* h, int64_t bl, const double* x, double* y, in
 }
 
 }  // extern "C"
+
+// ---- io (io.hpp:14-20): Matrix Market -> CsrMatrix via CooMatrix ------------
+#include "hdc/io.hpp"
+extern "C" int refc_read_matrix_market(const char* path, void** out) {
+    try {
+        *out = new RefCsr{CsrMatrix::from_coo(hdc::io::read_matrix_market(std::string(path)))};
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        return fail(e, -1);
+    } catch (const std::out_of_range& e) {
+        return fail(e, -2);
+    } catch (const std::overflow_error& e) {
+        return fail(e, -3);
+    } catch (const std::exception& e) {
+        return fail(e, -4);
+    }
+}

@@ -440,6 +440,22 @@ hdcg_status hdcg_upload_hdc(int64_t n, int64_t n_diag, const int32_t* offsets, c
     });
 }
 
+hdcg_status hdcg_read_matrix_market(const char* path, hdcg_matrix* out) {
+    return guard([&] {
+        if (!path || !out) fail(HDCG_ERR_INVALID_ARGUMENT, "null argument");
+        const int dev = use_device();
+        Matrix* m = new_matrix(dev);
+        try {
+            read_matrix_market(path, m);
+        } catch (...) {
+            matrix_release(m);
+            throw;
+        }
+        account(m);
+        *out = wrap(m);
+    });
+}
+
 hdcg_status hdcg_free(hdcg_matrix h) {
     return guard([&] { matrix_release(reinterpret_cast<Matrix*>(h)); });
 }

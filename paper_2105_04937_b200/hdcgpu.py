@@ -45,7 +45,7 @@ EXPORTS = (
     "hdcg_build_csr", "hdcg_upload_mhdc", "hdcg_upload_hdc", "hdcg_free", "hdcg_get_info",
     "hdcg_export", "hdcg_rates", "hdcg_census", "hdcg_spmv", "hdcg_spmv_host", "hdcg_spmv_slab",
     "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7", "hdcg_set_kernel_policy",
-    "hdcg_membench", "hdcg_analyze",
+    "hdcg_membench", "hdcg_analyze", "hdcg_read_matrix_market",
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
@@ -63,8 +63,12 @@ class CudaError(RuntimeError):
     pass
 
 
+class MatrixMarketError(RuntimeError):
+    """std::runtime_error of hdc::io::read_matrix_market (proj/src/io.cpp)."""
+
+
 _STATUS_EXC = {1: ValueError, 2: IndexError, 3: OverflowError, 4: CudaError, 5: NoDeviceError,
-               6: MemoryError}
+               6: MemoryError, 7: MatrixMarketError}
 
 
 class Info(C.Structure):
@@ -109,6 +113,7 @@ def lib():
         "hdcg_set_kernel_policy": [C.c_int],
         "hdcg_membench": [i64, C.c_int, C.c_int, C.c_int, C.POINTER(f64), C.POINTER(f64), vp],
         "hdcg_analyze": [i64, i64, vp, vp, vp, vp, C.c_int, vp, C.c_int, u, vp],
+        "hdcg_read_matrix_market": [C.c_char_p, C.POINTER(vp)],
         "hdcg_gen_uniform_pm1": [C.c_uint64, C.c_uint64, i64, i64, vp, vp],
         "hdcg_gen_laplacian7": [i64, i64, i64, i64, i64, vp, vp, vp, C.POINTER(i64), vp],
     }
@@ -300,6 +305,21 @@ def device_csr(m: CsrMatrix) -> DeviceCsr:
     check(lib().hdcg_build_csr(m.n, m.nnz, _ptr(m.row_ptr), _ptr(m.col_ind), _ptr(m.values),
                                m._flags(), None, C.byref(h)))
     return DeviceCsr(h.value)
+
+
+def read_matrix_market(path: str) -> DeviceCsr:
+    """hdc::io::read_matrix_market + CsrMatrix::from_coo (io.cpp:69-121,
+    formats.cpp:19-88): parsed on the host threads, normalised on the device;
+    the result is a device-resident CSR (see csr_from_device for host arrays)."""
+    h = _new_handle()
+    check(lib().hdcg_read_matrix_market(os.fsencode(path), C.byref(h)))
+    return DeviceCsr(h.value)
+
+
+def csr_from_device(d: DeviceCsr) -> CsrMatrix:
+    """Host copy of a device CSR (row_ptr int32, as index_t)."""
+    e = d.export()
+    return CsrMatrix(d.n, e["rest_values"], e["rest_col_ind"], e["rest_row_ptr"])
 
 
 def rates(m: DeviceMatrix) -> HybridRates:
