@@ -726,7 +726,7 @@ def test_matrix_market_large_parallel_parse(tmp_path, port):
     p = tmp_path / "big.mtx"
     with open(p, "w") as f:
         f.write(f"%%MatrixMarket matrix coordinate real general\n{n} {n} {m}\n")
-        f.writelines(f"{a} {b} {w!r}\n" for a, b, w in zip(r, c, v))
+        f.writelines(f"{a} {b} {float(w)!r}\n" for a, b, w in zip(r, c, v))
     got = H.csr_from_device(H.read_matrix_market(str(p)))
     want = synth.coo_to_csr(n, r - 1, c - 1, v)
     assert np.array_equal(got.row_ptr.astype(np.int64), want[0])
