@@ -20,7 +20,7 @@ namespace hdcg {
 
 namespace {
 
-constexpr int PIPE_CHUNKS = 8;
+constexpr int PIPE_CHUNKS = 32;
 
 // per tile: highest global column any of its rows reads (-1: none)
 __global__ void tile_xhi_kernel(int64_t n_tiles, int64_t tpb, int64_t bpt, int64_t tile_rows_n, int64_t bl,

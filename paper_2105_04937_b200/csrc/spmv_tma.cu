@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(CONSUMERS) rest_kernel(const TmaArgs a, int64_
     if (lo + threadIdx.x < hi) a.y[lo + threadIdx.x] = acc[0];
 }
 
-template <int R, bool SCALE, bool NORM>
+// REST: 0 no remainder, 1 remainder summed here (fused), 2 remainder sums already in y
+template <int R, bool SCALE, bool NORM, int REST>
 __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
     constexpr int XG = XGROUP_ROWS / R;  // x registers per thread stay at XGROUP_ROWS doubles
@@ -287,10 +288,10 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
 
         // CSR remainder first (stored order).  Either fused here (few remainder
         // entries) or already summed into y by rest_kernel (remainder-heavy matrices).
-        if (a.init_y) {
+        if constexpr (REST == 2) {
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = t0 + r < rows ? a.y[i0 + r] : 0.0;
-        } else if (a.has_rest) {
+        } else if constexpr (REST == 1) {
             warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
                                 S.scratch + warp * WPASS, acc);
         }
@@ -394,9 +395,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     }
 }
 
-template <int R, bool SCALE, bool NORM>
+template <int R, bool SCALE, bool NORM, int REST>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
-    auto k = spmv_tma_kernel<R, SCALE, NORM>;
+    auto k = spmv_tma_kernel<R, SCALE, NORM, REST>;
     static bool configured = false;  // per instantiation
     if (!configured) {
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -405,15 +406,22 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     k<<<grid, THREADS, smem, st>>>(a);
 }
 
+template <int R, int REST>
+void launch_rr(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
+    if (scale) {
+        if (norm) launch_one<R, true, true, REST>(a, grid, smem, st);
+        else launch_one<R, true, false, REST>(a, grid, smem, st);
+    } else {
+        if (norm) launch_one<R, false, true, REST>(a, grid, smem, st);
+        else launch_one<R, false, false, REST>(a, grid, smem, st);
+    }
+}
+
 template <int R>
 void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
-    if (scale) {
-        if (norm) launch_one<R, true, true>(a, grid, smem, st);
-        else launch_one<R, true, false>(a, grid, smem, st);
-    } else {
-        if (norm) launch_one<R, false, true>(a, grid, smem, st);
-        else launch_one<R, false, false>(a, grid, smem, st);
-    }
+    if (a.init_y) launch_rr<R, 2>(a, grid, smem, scale, norm, st);
+    else if (a.has_rest) launch_rr<R, 1>(a, grid, smem, scale, norm, st);
+    else launch_rr<R, 0>(a, grid, smem, scale, norm, st);
 }
 
 int sm_count() {

@@ -8,7 +8,7 @@ timeout 300 python scripts/diag_c3.py 4194304 > gpurun_out/diag.log 2>&1
 run() {  # label, workload, env...
   local label=$1; shift; local w=$1; shift
   env "$@" timeout 300 python bench.py --no-cpu-baseline --workload $w --steps 10 --warmup 3 2>/dev/null | tail -1 | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$label', '$w', d['value'], d['roofline']['frac'])" >> gpurun_out/ab.log
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$label', '$w', d['value'], d['roofline']['frac'], 'e2e', d['e2e']['value'])" >> gpurun_out/ab.log
 }
 for w in c1 c4 c2 c3; do
   run default $w
