@@ -200,10 +200,13 @@ hdcg_status hdcg_spmv_slab(hdcg_matrix m, const double* x_local, double* y, int6
                            int64_t block_end, const double* x_scale, double* tile_sumsq,
                            void* stream);
 
-/* Kernel selection (process-wide): 0 = automatic (the TMA-fed persistent kernel
- * for even bl >= 256, the general kernel otherwise), 1 = general kernel only,
- * 2 = TMA kernel only (ineligible shapes then fail with INVALID_ARGUMENT).
- * Both produce bitwise identical y and tile sums; this exists for testing. */
+/* Kernel selection (process-wide): policy & 3 = 0 automatic (the TMA-fed
+ * persistent kernel for even bl >= 256, the general kernel otherwise), 1 general
+ * kernel only, 2 TMA kernel only (ineligible shapes then fail with
+ * INVALID_ARGUMENT); policy >> 4 = how the TMA kernel reads the CSR remainder:
+ * 0 default, 1 consumers load it from global memory, 2 a separate kernel sums
+ * it into y first, 3 the producer stages it through the TMA ring.  All produce
+ * bitwise identical y and tile sums; this exists for testing. */
 hdcg_status hdcg_set_kernel_policy(int policy);
 
 /* Deterministic pairwise-tree sum of vals[0..count) (padded with +0.0 to a

@@ -108,6 +108,7 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st);
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
+extern int g_rest_mode;      // TMA kernel remainder mode (hdcg_set_kernel_policy), 0 default
 // Matrix Market ingestion (mmio.cu)
 void read_matrix_market(const char* path, Matrix* m);
 int64_t coo_dedup_to_csr(const int64_t* skeys, const double* svals, int64_t total, int64_t n, Matrix* m,

@@ -37,6 +37,7 @@ namespace hdcg {
 constexpr int SPMV_THREADS = 256;
 
 int g_kernel_policy = 0;  // 0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA only
+int g_rest_mode = 0;      // TMA kernel remainder: 0 default, 1 global loads, 2 rest_kernel first, 3 staged
 constexpr int REST_CHUNK = 1024;  // doubles of staged remainder products
 constexpr int SEG_UNROLL = 8;
 

@@ -96,7 +96,8 @@ struct TmaArgs {
     int tile_begin, tile_end;
     int nstage;
     int has_rest;
-    int init_y;  // remainder sums already in y (rest_kernel ran first)
+    int init_y;       // remainder sums already in y (rest_kernel ran first)
+    int rest_staged;  // the producer stages the remainder through the ring
     int y_vec_ok;
 };
 
@@ -147,7 +148,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
 // coalesced (evict-first), gather x for PER entries each (independent loads in
 // flight), leave the products in the warp's scratch, and each lane then adds its
 // rows' products sequentially.  Warp-synchronous.
-template <int R, bool SCALE>
+template <int R, bool SCALE, int PER = (R == 4 ? 4 : 8)>
 __device__ __forceinline__ void warp_rest(const int32_t* __restrict__ rest_rp, const int32_t* __restrict__ rest_col,
                                           const double* __restrict__ rest_val, const double* __restrict__ x,
                                           int64_t row0, double sc, int64_t lo, int64_t hi, int warp, int lane,
@@ -166,9 +167,7 @@ __device__ __forceinline__ void warp_rest(const int32_t* __restrict__ rest_rp, c
         kb[r] = ok ? __ldg(rest_rp + i0 + r) : 0;
         ke[r] = ok ? __ldg(rest_rp + i0 + r + 1) : 0;
     }
-    constexpr int PER = R == 4 ? 4 : 8;  // entries per lane per pass (x gathers in flight)
-    constexpr int PASS = 32 * PER;
-    static_assert(PASS <= WPASS, "scratch too small");
+    constexpr int PASS = 32 * PER;  // PER entries per lane per pass (x gathers in flight); scratch >= PASS
     for (int c = e_lo; c < e_hi; c += PASS) {
         int32_t cl[PER];
         double vl[PER], xl[PER];
@@ -205,21 +204,111 @@ __device__ __forceinline__ void warp_rest(const int32_t* __restrict__ rest_rp, c
 // then starts each row from y -- the same operations in the same order.
 // It only writes y, so its row mapping is free: one row per lane (a warp's 32 rows
 // usually fit one pass of 8 gathers per lane), 256 rows per CTA, many CTAs per SM.
-template <bool SCALE>
-__global__ void __launch_bounds__(CONSUMERS) rest_kernel(const TmaArgs a, int64_t row_lo, int64_t row_hi) {
-    __shared__ double scratch[CONSUMER_WARPS * WPASS];
-    const int64_t lo = row_lo + (int64_t)blockIdx.x * CONSUMERS;
-    const int64_t hi = min(lo + CONSUMERS, row_hi);
+template <bool SCALE, int MINB, int RR, int PER>
+__global__ void __launch_bounds__(CONSUMERS, MINB) rest_kernel(const TmaArgs a, int64_t row_lo, int64_t row_hi) {
+    __shared__ double scratch[CONSUMER_WARPS * 32 * PER];
+    const int64_t lo = row_lo + (int64_t)blockIdx.x * (CONSUMERS * RR);
+    const int64_t hi = min(lo + CONSUMERS * RR, row_hi);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
-    double acc[1] = {0.0};
-    warp_rest<1, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo, hi, warp, lane,
-                        scratch + warp * WPASS, acc);
-    if (lo + threadIdx.x < hi) a.y[lo + threadIdx.x] = acc[0];
+    double acc[RR];
+#pragma unroll
+    for (int r = 0; r < RR; ++r) acc[r] = 0.0;
+    warp_rest<RR, SCALE, PER>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo, hi, warp, lane,
+                              scratch + warp * 32 * PER, acc);
+    const int64_t i0 = lo + RR * threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < RR; ++r)
+        if (i0 + r < hi) a.y[i0 + r] = acc[r];
 }
 
-// REST: 0 no remainder, 1 remainder summed here (fused), 2 remainder sums already in y
+// Remainder entries per ring stage when the producer stages them (REST == 3): a
+// stage holds TILE doubles; ES values (8 B) + ES columns (4 B), ES a multiple of 32.
+template <int R>
+__host__ __device__ constexpr int rest_stage_entries() {
+    return (CONSUMERS * R * 8 / 12) / 32 * 32;
+}
+
+// Staged remainder (REST == 3): the producer has copied the tile's remainder
+// entries [e_lo & ~3, (e_hi + 3) & ~3) into consecutive ring stages with TMA
+// (values, then columns, in each stage).  Each warp takes, stage by stage, the
+// part of its own rows' entries that lies in the stage: columns and values come
+// from shared memory, x is gathered (the only global loads left on this path,
+// PER per lane in flight), products go to the warp's scratch and each lane adds
+// its rows' products in stored order.  Every warp waits for and releases every
+// rest stage of the tile (the ring is shared).
+template <int R, bool SCALE>
+__device__ __forceinline__ void staged_rest(const TmaArgs& a, const Smem& S, double sc, int64_t lo, int64_t hi,
+                                            int e_lo, int e_hi, int warp, int lane, int& cs, uint32_t& cphase,
+                                            double (&acc)[R]) {
+    constexpr int TILE = CONSUMERS * R;
+    constexpr int ES = rest_stage_entries<R>();
+    constexpr int PER = R == 4 ? 4 : 8;
+    constexpr int PASS = 32 * PER;
+    static_assert(PASS <= WPASS, "scratch too small");
+    const int t0 = R * (warp * 32 + lane);
+    const int rows = (int)(hi - lo);
+    const int64_t i0 = lo + t0;
+    const int64_t w_lo = min(lo + (int64_t)warp * 32 * R, hi);
+    const int64_t w_hi = min(w_lo + 32 * R, hi);
+    const int we0 = __ldg(a.rest_rp + w_lo), we1 = __ldg(a.rest_rp + w_hi);
+    int kb[R], ke[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const bool ok = t0 + r < rows;
+        kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
+        ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
+    }
+    double* scratch = S.scratch + warp * WPASS;
+    const int c_end = (e_hi + 3) & ~3;
+    for (int c = e_lo & ~3; c < c_end; c += ES) {
+        const int n = min(ES, c_end - c);
+        mbar_wait(&S.full[cs], cphase);
+        const double* sval = S.ring + cs * TILE;
+        const int32_t* scol = reinterpret_cast<const int32_t*>(sval + ES);
+        const int q0 = max(we0, c), q1 = min(we1, c + n);
+        for (int p = q0; p < q1; p += PASS) {
+            double xl[PER], vl[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const int q = p + lane + 32 * j;
+                xl[j] = 0.0;
+                vl[j] = 0.0;
+                if (q < q1) {
+                    vl[j] = sval[q - c];
+                    xl[j] = __ldg(a.x + ((int64_t)scol[q - c] - a.row0));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                double xv = xl[j];
+                if (SCALE) xv = __dmul_rn(xv, sc);
+                scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
+            }
+            __syncwarp();
+            const int pe = min(q1, p + PASS);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int p0 = max(kb[r], p), p1 = min(ke[r], pe);
+                for (int u = p0; u < p1; ++u) acc[r] = __dadd_rn(acc[r], scratch[u - p]);
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[cs]);
+        if (++cs == a.nstage) {
+            cs = 0;
+            cphase ^= 1u;
+        }
+    }
+}
+
+// REST: 0 no remainder, 1 remainder summed here from global memory (fused),
+// 2 remainder sums already in y (rest_kernel ran first), 3 remainder staged
+// through the ring by the producer (staged_rest)
 template <int R, bool SCALE, bool NORM, int REST>
 __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
@@ -249,6 +338,26 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R>(a, tile);
             if (g.lo >= g.hi) continue;
+            if constexpr (REST == 3) {
+                constexpr int ES = rest_stage_entries<R>();
+                const int e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
+                const int c_end = (e_hi + 3) & ~3;
+                if (e_hi > e_lo) {
+                    for (int c = e_lo & ~3; c < c_end; c += ES) {
+                        const uint32_t n = (uint32_t)min(ES, c_end - c);
+                        if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
+                        mbar_expect_tx(&S.full[ps], n * 12u);
+                        double* dst = S.ring + ps * TILE;
+                        bulk_g2s(dst, a.rest_val + c, n * 8u, &S.full[ps], policy);
+                        bulk_g2s(dst + ES, a.rest_col + c, n * 4u, &S.full[ps], policy);
+                        if (++ps == NS) {
+                            ps = 0;
+                            pphase ^= 1u;
+                            p_wrapped = true;
+                        }
+                    }
+                }
+            }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
             const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
             const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
@@ -294,6 +403,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         } else if constexpr (REST == 1) {
             warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
                                 S.scratch + warp * WPASS, acc);
+        } else if constexpr (REST == 3) {
+            const int e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
+            if (e_hi > e_lo) staged_rest<R, SCALE>(a, S, sc, g.lo, g.hi, e_lo, e_hi, warp, lane, cs, cphase, acc);
         }
 
         // diagonal segments, stored order
@@ -420,6 +532,7 @@ void launch_rr(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, c
 template <int R>
 void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if (a.init_y) launch_rr<R, 2>(a, grid, smem, scale, norm, st);
+    else if (a.has_rest && a.rest_staged) launch_rr<R, 3>(a, grid, smem, scale, norm, st);
     else if (a.has_rest) launch_rr<R, 1>(a, grid, smem, scale, norm, st);
     else launch_rr<R, 0>(a, grid, smem, scale, norm, st);
 }
@@ -466,10 +579,17 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.init_y = 0;
+    a.rest_staged = 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
-    // Remainder-heavy (>= 1 entry per 4 rows on average): sum it in rest_kernel first.
-    static const int env_split = getenv("HDCG_REST_SPLIT") ? atoi(getenv("HDCG_REST_SPLIT")) : -1;
-    const bool split = env_split >= 0 ? (env_split > 0 && a.has_rest) : (m.nnz_rest * 4 >= m.n_rows && a.has_rest);
+    // Remainder mode (hdcg_set_kernel_policy / HDCG_REST_MODE override the default):
+    // 2 summed first by rest_kernel -- the default for remainder-heavy matrices (>= 1
+    // entry per 4 rows); 1 loaded from global memory by the consumers -- the default
+    // otherwise; 3 staged through the ring by the producer.
+    static const int env_mode = getenv("HDCG_REST_MODE") ? atoi(getenv("HDCG_REST_MODE")) : 0;
+    const int req = g_rest_mode ? g_rest_mode : env_mode;
+    const int mode = req >= 1 && req <= 3 ? req : (m.nnz_rest * 4 >= m.n_rows ? 2 : 1);
+    a.rest_staged = a.has_rest && mode == 3;
+    const bool split = a.has_rest && mode == 2;
     if (split) {
         // rows covered by the tile range (tiles are contiguous in rows)
         int64_t r0, r1, dummy;
@@ -477,9 +597,11 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         tile_rows(tile_end - 1, t.tiles_per_block, 0, t.tile_rows, m.bl, m.n_rows, &dummy, &r1);
         r0 = std::min(r0, m.n_rows);
         if (r1 > r0) {
+            // 5 CTAs/SM (48 registers), one row per lane, 8 gathers per lane in flight:
+            // the best of the variants measured (profiles/README.md, v8)
             const unsigned nb = (unsigned)ceil_div(r1 - r0, CONSUMERS);
-            if (x_scale) rest_kernel<true><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
-            else rest_kernel<false><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
+            if (x_scale) rest_kernel<true, 5, 1, 8><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
+            else rest_kernel<false, 5, 1, 8><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
             HDCG_LAUNCH_CHECK("rest_kernel");
         }
         a.has_rest = 0;

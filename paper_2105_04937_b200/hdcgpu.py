@@ -49,6 +49,7 @@ EXPORTS = (
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
+REST_DEFAULT, REST_GLOBAL, REST_SPLIT, REST_STAGED = 0, 1, 2, 3
 
 
 class LibraryMissing(ImportError):
@@ -532,6 +533,8 @@ def membench(n: int, mode: str = "direct", n_loops: int = 20, n_ites: int = 1000
     return Measurement(best.value, loops.tolist(), bps.value)
 
 
-def set_kernel_policy(policy: int):
-    """0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA kernel only."""
-    check(lib().hdcg_set_kernel_policy(policy))
+def set_kernel_policy(policy: int, rest_mode: int = 0):
+    """policy: 0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA kernel only.
+    rest_mode (TMA kernel's CSR remainder): 0 default, 1 global loads, 2 summed first
+    by a separate kernel, 3 staged through the TMA ring."""
+    check(lib().hdcg_set_kernel_policy(policy + 16 * rest_mode))

@@ -20,8 +20,9 @@ for bl in (1024, 8192):
     ref = P.to_mhdc(rp, col, val, 0.6, bl)
     yref = P.spmv_mhdc(ref, x, 0)
     m = H.to_mhdc(A, 0.6, bl)
-    for pol in (H.POLICY_GENERAL, H.POLICY_AUTO):
-        H.set_kernel_policy(pol)
+    for pol, rm in ((H.POLICY_GENERAL, 0), (H.POLICY_TMA, H.REST_SPLIT), (H.POLICY_TMA, H.REST_STAGED),
+                    (H.POLICY_TMA, H.REST_GLOBAL)):
+        H.set_kernel_policy(pol, rm)
         for rep in range(3):
             y = H.spmv_mhdc(m, x)
             bad = np.nonzero(y.view(np.int64) != yref.view(np.int64))[0]
@@ -31,5 +32,5 @@ for bl in (1024, 8192):
                 info = (f" first row {i} (tile {i // 512}, row-in-tile {i % 512}), got {y[i]!r} want {yref[i]!r}, "
                         f"rest entries {ref.rest_rp[i + 1] - ref.rest_rp[i]}, rest_rp {ref.rest_rp[i]}; "
                         f"rows: {bad[:12].tolist()}")
-            print(f"bl={bl} policy={pol} rep={rep}: {bad.size} bad rows{info}", flush=True)
+            print(f"bl={bl} policy={pol} rest={rm} rep={rep}: {bad.size} bad rows{info}", flush=True)
     H.set_kernel_policy(H.POLICY_AUTO)

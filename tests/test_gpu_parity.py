@@ -557,22 +557,36 @@ def test_reference_acceptance_through_gpu_shim():
     assert "all 8 criteria passed" in r.stdout
 
 
-def test_remainder_fused_and_split_paths(port):
-    """The TMA kernel sums a sparse remainder in-kernel (fused) and a heavy one in a
-    separate rest_kernel first (split); both must be bitwise equal to the oracle."""
+@pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT, H.REST_STAGED])
+def test_remainder_paths(port, rest_mode):
+    """The TMA kernel's three ways of summing the CSR remainder (consumers load it from
+    global memory; a separate rest_kernel sums it into y first; the producer stages it
+    through the TMA ring) must all be bitwise equal to the oracle, sparse and heavy."""
+    H.set_kernel_policy(H.POLICY_TMA, rest_mode)
+    try:
+        _remainder_cases(port)
+    finally:
+        H.set_kernel_policy(H.POLICY_AUTO)
+
+
+def _remainder_cases(port):
     rng = np.random.default_rng(17)
     rp, col, val = synth.laplacian7(32, 32, 32)
     n = 32 ** 3
     i = np.repeat(np.arange(n), np.diff(rp))
-    for extra in (200, 20000):  # n/4 = 8192 separates the two paths
-        r = rng.integers(0, n, extra)
+    for extra in (200, 20000, 200000, -1):
+        if extra < 0:  # a few very long rows: their entries span several ring stages
+            r = np.repeat(np.array([5, 511, 512, 7000, n - 1]), 3000)
+            extra = r.size
+        else:
+            r = rng.integers(0, n, extra)
         c = rng.integers(0, n, extra)
         rows = np.concatenate([i, r])
         cols = np.concatenate([col.astype(np.int64), c])
         vals = np.concatenate([val, rng.uniform(-1, 1, extra)])
         rp2, col2, val2 = synth.coo_to_csr(n, rows, cols, vals)
         x = synth.x_vector(n, 3)
-        for bl in (1024, 4096, 512):
+        for bl in (1024, 4096, 512, 384):
             ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
             m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
             assert_mhdc_equal(m, ref, (extra, bl))
