@@ -65,8 +65,12 @@ def kernel_name(info, scale=False, norm=False):
     """Which SpMV kernel the library launches for this matrix (spmv.cu::tiling_of)."""
     r = info.tile_rows // 256
     tma = info.bl % 2 == 0 and info.bl >= 256
-    name = "spmv_tma_kernel" if tma else "spmv_kernel"
-    return f"hdcg::{name}<{r},{str(scale).lower()},{str(norm).lower()}>"
+    if not tma:
+        return f"hdcg::spmv_kernel<{r},{str(scale).lower()},{str(norm).lower()}>"
+    # remainder mode (spmv_tma.cu::spmv_tma_launch): 0 none, 1 fused, 2 rest_kernel first
+    rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
+    name = f"hdcg::spmv_tma_kernel<{r},{str(scale).lower()},{str(norm).lower()},{rest}>"
+    return name + (" (+ rest_kernel)" if rest == 2 else "")
 
 
 def load_peaks():
