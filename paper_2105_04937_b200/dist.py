@@ -12,7 +12,7 @@ Power iteration (config 4: x <- y/||y||) per step k, on rank r:
      NVLink, torch.distributed) -- overlapped with
   3. the interior blocks;
   4. per-tile sums of y_i^2 (fused into the SpMV) -> local pairwise tree ->
-     all-gather of the rank roots -> top tree -> s_k = 1/sqrt(sum).
+     all-gather of the rank roots -> top tree (the same tree kernel) -> s_k = 1/sqrt(sum).
 The scale s is applied inside the next SpMV's x loads, so no separate
 normalisation pass streams y again.  Every row is owned by one rank and keeps
 its per-row operation order, so y is bitwise independent of the number of
@@ -154,8 +154,9 @@ class SlabPowerIteration:
             HaloExchange.wait(reqs)
             local = self.c.tree(self.tiles)
             dist.all_gather_into_tensor(self.roots, local[0:1].contiguous())
-            total = pairwise_tree(self.roots)[0]
-            self.red = torch.stack([total, 1.0 / torch.sqrt(total)])
+            # the top of the tree over the rank roots: the same padded pairwise tree,
+            # one launch on the device (stream-ordered after the all-gather)
+            self.red = self.c.tree(self.roots)
             self.scale.copy_(self.red[1:2])
         self.bufs.reverse()
         return self.red
