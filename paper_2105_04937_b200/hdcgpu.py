@@ -31,7 +31,8 @@ from typing import NamedTuple
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhdcgpu.so")
+# HDCG_LIBRARY: another in-tree build of the same library (same-box A/B of kernel versions)
+LIB_PATH = os.environ.get("HDCG_LIBRARY") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhdcgpu.so")
 
 HDCG_INPUT_DEVICE = 1
 HDCG_VALIDATE = 2
