@@ -170,6 +170,17 @@ def cpu_sample(workload):
     return synth.quasi_diag(1 << 22, seed=4), 8192, "config-3 sample: n = 2^22 (1/4 of the rows)"
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_cpu_reference(workload, fmt, steps, warmup):
     """Times the reference's CPU kernel with all host threads.  Returns a dict."""
     (rp, col, val), bl, sample = cpu_sample(workload)
@@ -205,7 +216,14 @@ def run_cpu_reference(workload, fmt, steps, warmup):
         call()
         times.append(time.perf_counter() - t0)
     t = statistics.mean(times)
-    return {"value": 2.0 * nnz / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind,
+    host = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    if kind == "reference":  # the reference's own membench (bench.cpp:68-110), direct mode, all threads
+        try:
+            bps, _ = R.membench(1 << 24, "direct", n_loops=3, n_ites=5)
+            host["membench_direct_gbs"] = round(bps / 1e9, 2)
+        except Exception as e:  # noqa: BLE001 - reported, not fatal
+            host["membench_error"] = str(e)
+    return {"value": 2.0 * nnz / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind, "host": host,
             "sample": f"{sample}, {fmt} theta={THETA} bl={bl}, nnz={nnz}, {steps} timed calls "
                       f"(mean {t * 1e3:.2f} ms) after {warmup} warm-up",
             "ms_per_call": t * 1e3, "best_ms": min(times) * 1e3}

@@ -222,6 +222,8 @@ class Ref:
         L.refc_time_spmv.argtypes = [C.c_int, vp, C.c_int64, _f64p, _f64p, C.c_int64, C.c_int,
                                      C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.refc_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(vp)]
+        L.refc_membench.argtypes = [C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]
 
     def _check(self, rc):
         if rc != 0:
@@ -340,6 +342,13 @@ class Ref:
         self._check(self.lib.refc_spmv(self.KIND[kernel], hd.h, bl, _c(x, np.float64), y, hd.n,
                                        workers))
         return y
+
+    def membench(self, n, mode="direct", n_loops=3, n_ites=5, workers=0):
+        """The reference's host membench (bench.cpp:68-110): (bytes_per_s, best_time_s)."""
+        bps, best = C.c_double(), C.c_double()
+        self._check(self.lib.refc_membench(n, 0 if mode == "direct" else 1, n_loops, n_ites, workers,
+                                           C.byref(bps), C.byref(best)))
+        return bps.value, best.value
 
     def time_spmv(self, kernel, hd, x, bl=0, workers=0, n_loops=5, n_ites=10):
         y = np.empty(hd.n, dtype=np.float64)

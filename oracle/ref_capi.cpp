@@ -250,6 +250,22 @@ int refc_time_spmv(int kind, void* h, int64_t bl, const double* x, double* y, in
     });
 }
 
+// The reference's streaming micro-benchmark (bench.hpp:33-46, bench.cpp:68-110):
+// mode 0 direct (32 B/element), 1 indirect (36 B/element).
+int refc_membench(int64_t n, int mode, int n_loops, int n_ites, int workers, double* bytes_per_s,
+                  double* best_s) {
+    return guarded([&] {
+        bench::TimingConfig cfg;
+        cfg.n_loops = n_loops;
+        cfg.n_ites = n_ites;
+        cfg.workers = workers;
+        const bench::Measurement m = bench::membench(static_cast<index_t>(n),
+                                                     mode ? bench::MemMode::indirect : bench::MemMode::direct, cfg);
+        *bytes_per_s = m.bytes_per_s;
+        *best_s = m.best_time_s;
+    });
+}
+
 }  // extern "C"
 
 // ---- io (io.hpp:14-20): Matrix Market -> CsrMatrix via CooMatrix ------------
