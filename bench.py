@@ -11,7 +11,7 @@ N grows -> "scaling": "strong".  The matrix (38.6 GB of algorithmic traffic per
 step) is far larger than L2 (126 MB), so no L2 flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c4|c1|c2|c3] [--format mhdc|hdc] [--bl B]
+                    [--workload c4|c1|c2|c3] [--format mhdc|hdc|csr] [--bl B]
 
 Other workloads (c1..c3, single SpMV steps) are for DESIGN.md / profiling.
 --impl reference times the reference's own CPU spmv_mhdc (oracle/_ref, the
@@ -190,7 +190,10 @@ def run_cpu_reference(workload, fmt, steps, warmup):
         from oracle.oracle import Ref
         R = Ref()
         kind = "reference"
-        h = R.hdc_handle(rp, col, val, THETA) if fmt == "hdc" else R.mhdc_handle(rp, col, val, THETA, bl)
+        if fmt == "csr":
+            h = R.csr(rp, col, val)
+        else:
+            h = R.hdc_handle(rp, col, val, THETA) if fmt == "hdc" else R.mhdc_handle(rp, col, val, THETA, bl)
         cores = R.max_threads()
 
         y = np.zeros_like(x)
@@ -207,7 +210,10 @@ def run_cpu_reference(workload, fmt, steps, warmup):
         y = np.zeros_like(x)
 
         def call():
-            P.spmv_mhdc(m, x, 0, out=y)
+            if fmt == "csr":
+                y[:] = P.spmv_csr(rp, col, val, x, 0)
+            else:
+                P.spmv_mhdc(m, x, 0, out=y)
     for _ in range(warmup):
         call()
     times = []
@@ -420,7 +426,12 @@ def run_ours_single(a):
     n = len(rp) - 1
     A = H.CsrMatrix(n, val, col, rp.astype(np.int32))
     t0 = time.perf_counter()
-    m = H.to_hdc(A, THETA, validate=False) if a.format == "hdc" else H.to_mhdc(A, THETA, bl, validate=False)
+    if a.format == "csr":  # the paper's baseline format (RP(M-HDC/CSR))
+        m = H.device_csr(A)
+    elif a.format == "hdc":
+        m = H.to_hdc(A, THETA, validate=False)
+    else:
+        m = H.to_mhdc(A, THETA, bl, validate=False)
     t_build = time.perf_counter() - t0
     info = m.info
     x = torch.from_numpy(synth.x_vector(n, seed)).cuda()
@@ -455,14 +466,16 @@ def run_ours_single(a):
         "metric": METRIC, "value": round(2 * nnz / (ms * 1e-3) / 1e9, 2), "unit": UNIT, "n_gpus": 1,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{label}, {a.format} theta=0.6" + ("" if a.format == "hdc" else f" bl={bl}"),
+        "config": {"workload": f"{label}, {a.format}" + ("" if a.format == "csr" else " theta=0.6")
+                   + ("" if a.format != "mhdc" else f" bl={bl}"),
                    "n": n, "nnz": nnz, "n_seg": info.n_seg, "nnz_rest": info.nnz_rest,
                    "dia_slots": info.dia_slots, "convert_s": round(t_build, 3),
                    "l2": "256 MB L2 flush before every timed launch"},
         "roofline": {"bound": "hbm", "achieved": round(bts / (ms * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(bts / (ms * 1e-3) / 1e9 / peak, 4),
                      "traffic": load_traffic(f"{a.workload}_{a.format}_bl{bl}"),
-                     "algorithmic_bytes_per_launch": bts, "peak_source": f"{peak_kind} hbm_gbs"},
+                     "algorithmic_bytes_per_launch": bts, "peak_source": f"{peak_kind} hbm_gbs",
+                     "kernel": kernel_name(info)},
         "e2e": {"value": round(2 * nnz / e2e / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n},
         "gpu_launches": a.steps,
@@ -497,7 +510,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c4", "c1", "c2", "c3"], default="c4")
-    ap.add_argument("--format", choices=["mhdc", "hdc"], default="mhdc")
+    ap.add_argument("--format", choices=["mhdc", "hdc", "csr"], default="mhdc")
     ap.add_argument("--bl", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args(argv)

@@ -200,8 +200,9 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 
 // One tiling for both kernels (spmv_kernel and spmv_tma_kernel), so per-tile
 // partial sums and block-range alignment do not depend on which one runs:
-//   bl % 4 == 0, >= 1024, <= 8 segments per block (stencil-like): 4 rows/thread,
-//                         1024-row tiles, ceil(bl/1024) tiles per block
+//   <= 8 segments per block (stencil-like) and bl % 4 == 0, >= 1024, or
+//   bl in {128, 256, 512}: 4 rows/thread, 1024-row tiles, ceil(bl/1024) tiles
+//                         per block (or 1024/bl whole blocks per tile)
 //   other even bl >= 512 : 2 rows/thread, 512-row tiles
 //   even bl in [256,512): 1 row/thread, 256-row tiles, 2 tiles per block
 //   even bl < 256      : 2 rows/thread, 512/bl whole blocks per tile
@@ -209,7 +210,9 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
     const bool even = m.bl % 2 == 0;
-    if (m.bl % 4 == 0 && m.bl >= 4 * SPMV_THREADS && m.max_seg_per_block <= 8) t.rows_per_thread = 4;
+    const int64_t t4 = 4 * SPMV_THREADS;
+    if (m.bl % 4 == 0 && m.max_seg_per_block <= 8 && (m.bl >= t4 || (m.bl >= 128 && t4 % m.bl == 0)))
+        t.rows_per_thread = 4;
     else if (even && (m.bl >= 2 * SPMV_THREADS || m.bl < SPMV_THREADS)) t.rows_per_thread = 2;
     else t.rows_per_thread = 1;
     t.tile_rows = (int64_t)SPMV_THREADS * t.rows_per_thread;

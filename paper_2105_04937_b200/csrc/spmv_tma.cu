@@ -24,8 +24,11 @@
 //   * y is stored once per tile (streaming store); the optional fused per-tile
 //     sum of squares has the same fixed reduction order as spmv.cu, with one
 //     consumer barrier per tile (double-buffered warp partials).
-// Used for even bl >= 256 (all BASELINE M-HDC configurations, HDC with even n);
-// other shapes take the general kernel in spmv.cu.
+// Used for even bl >= 256 (all BASELINE M-HDC configurations, HDC with even n)
+// and for small blocks that tile evenly (bl in {128, 256, 512} with R = 4: a
+// tile = G = 1024/bl whole blocks; ring stage j then carries segment j of each of the G blocks,
+// each warp's rows lie in one block); other shapes take the general kernel in
+// spmv.cu.
 #include <algorithm>
 #include <cstdlib>
 
@@ -92,7 +95,9 @@ struct TmaArgs {
     const double* x_scale;
     double* tile_sumsq;
     int64_t n_rows, n_cols, row0, bl;
-    int tiles_per_block;
+    int tiles_per_block;  // > 0: a tile is a part of one block
+    int blocks_per_tile;  // > 0: a tile is G whole blocks (bl < TILE, bl % (32 R) == 0)
+    int64_t n_blocks;
     int tile_begin, tile_end;
     int nstage;
     int has_rest;
@@ -106,9 +111,15 @@ struct Geo {
     int b;
 };
 
-template <int R>
+template <int R, bool MB>
 __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     Geo g;
+    if constexpr (MB) {  // G whole blocks: b = the first one
+        g.b = tile * a.blocks_per_tile;
+        g.b0 = g.lo = (int64_t)g.b * a.bl;
+        g.hi = min(g.lo + (int64_t)a.blocks_per_tile * a.bl, a.n_rows);
+        return g;
+    }
     g.b = tile / a.tiles_per_block;
     const int t = tile - g.b * a.tiles_per_block;
     g.b0 = (int64_t)g.b * a.bl;
@@ -309,7 +320,8 @@ __device__ __forceinline__ void staged_rest(const TmaArgs& a, const Smem& S, dou
 // REST: 0 no remainder, 1 remainder summed here from global memory (fused),
 // 2 remainder sums already in y (rest_kernel ran first), 3 remainder staged
 // through the ring by the producer (staged_rest)
-template <int R, bool SCALE, bool NORM, int REST>
+// MB: multi-block tiles (a.blocks_per_tile > 0), instantiated for R = 4 only
+template <int R, bool SCALE, bool NORM, int REST, bool MB>
 __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     constexpr int TILE = CONSUMERS * R;
     constexpr int XG = XGROUP_ROWS / R;  // x registers per thread stay at XGROUP_ROWS doubles
@@ -336,7 +348,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         uint32_t pphase = 0;     // parity of that stage's current use
         bool p_wrapped = false;  // every stage has been used once
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-            const Geo g = geo<R>(a, tile);
+            const Geo g = geo<R, MB>(a, tile);
             if (g.lo >= g.hi) continue;
             if constexpr (REST == 3) {
                 constexpr int ES = rest_stage_entries<R>();
@@ -357,6 +369,42 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                         }
                     }
                 }
+            }
+            if constexpr (MB) {
+                // stage j = segment j of each of the tile's blocks, block q's slots at
+                // q*bl (the tile-local row); blocks with fewer segments leave theirs unused
+                constexpr int GMAX = 8;  // TILE / bl <= TILE / (32 R) = 8
+                const int nbt = (int)min((int64_t)a.blocks_per_tile, a.n_blocks - g.b);
+                const int64_t last_len = min((int64_t)a.bl, a.n_rows - (int64_t)(g.b + nbt - 1) * a.bl);
+                int kst[GMAX], cnt[GMAX];
+                uint32_t pb[GMAX];
+                int J = 0;
+#pragma unroll
+                for (int q = 0; q < GMAX; ++q) {
+                    kst[q] = q < nbt ? __ldg(a.dia_ptr + g.b + q) : 0;
+                    cnt[q] = q < nbt ? __ldg(a.dia_ptr + g.b + q + 1) - kst[q] : 0;
+                    pb[q] = (uint32_t)(((q == nbt - 1 ? last_len : a.bl) + 1) & ~int64_t(1)) * 8u;
+                    J = max(J, cnt[q]);
+                }
+                for (int j = 0; j < J; ++j) {
+                    uint32_t bytes = 0;
+#pragma unroll
+                    for (int q = 0; q < GMAX; ++q)
+                        if (j < cnt[q]) bytes += pb[q];
+                    if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
+                    mbar_expect_tx(&S.full[ps], bytes);
+#pragma unroll
+                    for (int q = 0; q < GMAX; ++q)
+                        if (j < cnt[q])
+                            bulk_g2s(S.ring + ps * TILE + q * a.bl, a.seg + (int64_t)(kst[q] + j) * a.bl, pb[q],
+                                     &S.full[ps], policy);
+                    if (++ps == NS) {
+                        ps = 0;
+                        pphase ^= 1u;
+                        p_wrapped = true;
+                    }
+                }
+                continue;
             }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
             const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
@@ -384,7 +432,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     const int t0 = R * threadIdx.x;  // local row of this thread's first row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-        const Geo g = geo<R>(a, tile);
+        const Geo g = geo<R, MB>(a, tile);
         if (g.lo >= g.hi) {
             if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
             continue;
@@ -408,23 +456,41 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             if (e_hi > e_lo) staged_rest<R, SCALE>(a, S, sc, g.lo, g.hi, e_lo, e_hi, warp, lane, cs, cphase, acc);
         }
 
-        // diagonal segments, stored order
-        const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
+        // diagonal segments, stored order.  k0: this warp's block's first segment,
+        // nseg its count, J the number of ring stages the tile takes (the largest
+        // count over the tile's blocks; = nseg when the tile is inside one block).
+        // [k0, k1): the ring stages of the tile; [k0, kw): this warp's block's
+        // segments (MB: k1 - k0 is the largest segment count over the tile's
+        // blocks; otherwise kw = k1, the one block's segments).
+        int k0, k1, kw;
+        if constexpr (MB) {  // warp-uniform: bl % (32 R) == 0
+            const int64_t bw = (int64_t)g.b + t0 / (int)a.bl;
+            const int nbt = (int)min((int64_t)a.blocks_per_tile, a.n_blocks - g.b);
+            k0 = bw < a.n_blocks ? __ldg(a.dia_ptr + bw) : 0;
+            kw = bw < a.n_blocks ? __ldg(a.dia_ptr + bw + 1) : 0;
+            const int c = lane < nbt ? __ldg(a.dia_ptr + g.b + lane + 1) - __ldg(a.dia_ptr + g.b + lane) : 0;
+            k1 = k0 + __reduce_max_sync(0xffffffffu, c);
+        } else {
+            k0 = __ldg(a.dia_ptr + g.b);
+            k1 = kw = __ldg(a.dia_ptr + g.b + 1);
+        }
         const double* xrow = a.x + i0;
         const bool full = rows == TILE;  // warp-uniform: no per-row predicates needed
         for (int kb0 = k0; kb0 < k1; kb0 += 32) {
             // the next <= 32 offsets of the block: one coalesced load, then shuffles
             const int nk = min(32, k1 - kb0);
-            const int my_off = lane < nk ? __ldg(a.dia_off + kb0 + lane) : 0;
+            const int nko = MB ? min(32, kw - kb0) : nk;  // of which this warp's block has
+            const int my_off = lane < nko ? __ldg(a.dia_off + kb0 + lane) : 0;
             for (int kg = 0; kg < nk; kg += XG) {
                 const int ng = min(XG, nk - kg);  // warp-uniform
+                const int nv = MB ? min(ng, kw - kb0 - kg) : ng;  // of which this warp's block has
                 double xv[XG][R];
 #pragma unroll
                 for (int u = 0; u < XG; ++u) {
                     const int64_t o = __shfl_sync(0xffffffffu, my_off, (kg + u) & 31);
 #pragma unroll
                     for (int r = 0; r < R; ++r) xv[u][r] = 0.0;
-                    if (u < ng) {
+                    if (u < nv) {
                         if (full && g.lo + o >= xlo_valid && g.hi + o <= xhi_valid) {  // common case
 #pragma unroll
                             for (int r = 0; r < R; ++r) xv[u][r] = __ldg(xrow + r + o);
@@ -453,11 +519,13 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                         } else {
                             v[0] = st[0];
                         }
+                        if (u < nv) {
 #pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            double xx = xv[u][r];
-                            if (SCALE) xx = __dmul_rn(xx, sc);
-                            acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
+                            for (int r = 0; r < R; ++r) {
+                                double xx = xv[u][r];
+                                if (SCALE) xx = __dmul_rn(xx, sc);
+                                acc[r] = __dadd_rn(acc[r], __dmul_rn(v[r], xx));
+                            }
                         }
                         // Release the stage only once this thread's shared loads have
                         // delivered (acc depends on them), then order the warp's reads
@@ -507,9 +575,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     }
 }
 
-template <int R, bool SCALE, bool NORM, int REST>
+template <int R, bool SCALE, bool NORM, int REST, bool MB>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
-    auto k = spmv_tma_kernel<R, SCALE, NORM, REST>;
+    auto k = spmv_tma_kernel<R, SCALE, NORM, REST, MB>;
     static bool configured = false;  // per instantiation
     if (!configured) {
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -518,23 +586,31 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     k<<<grid, THREADS, smem, st>>>(a);
 }
 
-template <int R, int REST>
+template <int R, int REST, bool MB>
 void launch_rr(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if (scale) {
-        if (norm) launch_one<R, true, true, REST>(a, grid, smem, st);
-        else launch_one<R, true, false, REST>(a, grid, smem, st);
+        if (norm) launch_one<R, true, true, REST, MB>(a, grid, smem, st);
+        else launch_one<R, true, false, REST, MB>(a, grid, smem, st);
     } else {
-        if (norm) launch_one<R, false, true, REST>(a, grid, smem, st);
-        else launch_one<R, false, false, REST>(a, grid, smem, st);
+        if (norm) launch_one<R, false, true, REST, MB>(a, grid, smem, st);
+        else launch_one<R, false, false, REST, MB>(a, grid, smem, st);
     }
+}
+
+template <int R, bool MB>
+void launch_m(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
+    if (a.init_y) launch_rr<R, 2, MB>(a, grid, smem, scale, norm, st);
+    else if (a.has_rest && a.rest_staged) launch_rr<R, 3, MB>(a, grid, smem, scale, norm, st);
+    else if (a.has_rest) launch_rr<R, 1, MB>(a, grid, smem, scale, norm, st);
+    else launch_rr<R, 0, MB>(a, grid, smem, scale, norm, st);
 }
 
 template <int R>
 void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
-    if (a.init_y) launch_rr<R, 2>(a, grid, smem, scale, norm, st);
-    else if (a.has_rest && a.rest_staged) launch_rr<R, 3>(a, grid, smem, scale, norm, st);
-    else if (a.has_rest) launch_rr<R, 1>(a, grid, smem, scale, norm, st);
-    else launch_rr<R, 0>(a, grid, smem, scale, norm, st);
+    if constexpr (R == 4) {
+        if (a.blocks_per_tile > 0) return launch_m<4, true>(a, grid, smem, scale, norm, st);
+    }
+    launch_m<R, false>(a, grid, smem, scale, norm, st);
 }
 
 int sm_count() {
@@ -557,7 +633,9 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     if (m.nnz_rest > 0 && (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0)) return false;
     const Tiling t = tiling_of(m);
     const int R = t.rows_per_thread;
-    if (t.tiles_per_block <= 0 || t.tile_rows != (int64_t)CONSUMERS * R) return false;
+    if (t.tile_rows != (int64_t)CONSUMERS * R) return false;
+    // multi-block tiles: R = 4 (bl in {128, 256, 512}, tiling_of) only
+    if (t.tiles_per_block <= 0 && (R != 4 || t.blocks_per_tile <= 0 || m.bl % (32 * R) != 0)) return false;
     if (tile_end <= tile_begin) return true;
     TmaArgs a;
     a.dia_ptr = m.dia_ptr;
@@ -575,6 +653,8 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.row0 = m.row0;
     a.bl = m.bl;
     a.tiles_per_block = (int)t.tiles_per_block;
+    a.blocks_per_tile = (int)t.blocks_per_tile;
+    a.n_blocks = m.n_blocks;
     a.tile_begin = (int)tile_begin;
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
@@ -590,41 +670,48 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     const int mode = req >= 1 && req <= 3 ? req : (m.nnz_rest * 4 >= m.n_rows ? 2 : 1);
     a.rest_staged = a.has_rest && mode == 3;
     const bool split = a.has_rest && mode == 2;
-    if (split) {
+    auto rest_rows = [&](int64_t tb, int64_t te, cudaStream_t s) {
         // rows covered by the tile range (tiles are contiguous in rows)
         int64_t r0, r1, dummy;
-        tile_rows(tile_begin, t.tiles_per_block, 0, t.tile_rows, m.bl, m.n_rows, &r0, &dummy);
-        tile_rows(tile_end - 1, t.tiles_per_block, 0, t.tile_rows, m.bl, m.n_rows, &dummy, &r1);
+        tile_rows(tb, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m.bl, m.n_rows, &r0, &dummy);
+        tile_rows(te - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m.bl, m.n_rows, &dummy, &r1);
         r0 = std::min(r0, m.n_rows);
         if (r1 > r0) {
             // 5 CTAs/SM (48 registers), one row per lane, 8 gathers per lane in flight:
             // the best of the variants measured (profiles/README.md, v8)
             const unsigned nb = (unsigned)ceil_div(r1 - r0, CONSUMERS);
-            if (x_scale) rest_kernel<true, 5, 1, 8><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
-            else rest_kernel<false, 5, 1, 8><<<nb, CONSUMERS, 0, st>>>(a, r0, r1);
+            if (x_scale) rest_kernel<true, 5, 1, 8><<<nb, CONSUMERS, 0, s>>>(a, r0, r1);
+            else rest_kernel<false, 5, 1, 8><<<nb, CONSUMERS, 0, s>>>(a, r0, r1);
             HDCG_LAUNCH_CHECK("rest_kernel");
         }
-        a.has_rest = 0;
-        a.init_y = 1;
-    }
+    };
     // ring of segment slices: ~64 KB per CTA, 3 CTAs per SM (tunable for profiling)
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
-    const int want_ctas = env_ctas > 0 ? env_ctas : 3;
-    const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
-    const size_t fixed = smem_bytes(R, 0, a.has_rest);
-    const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
-    a.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
-    const size_t smem = smem_bytes(R, a.nstage, a.has_rest);
-    const int fit = (int)((227 * 1024) / (smem + 1024));
-    const int per_sm = std::max(1, std::min(want_ctas, fit));
-    const int64_t n_tiles = tile_end - tile_begin;
-    const int64_t cap = (int64_t)sm_count() * per_sm;
-    const int grid = (int)(n_tiles < cap ? n_tiles : cap);
-    if (R == 4) launch_r<4>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
-    else if (R == 2) launch_r<2>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
-    else launch_r<1>(a, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, st);
-    HDCG_LAUNCH_CHECK("spmv_tma_kernel");
+    auto tma = [&](const TmaArgs& base, int64_t tb, int64_t te, int want_ctas, cudaStream_t s) {
+        TmaArgs b = base;
+        b.tile_begin = (int)tb;
+        b.tile_end = (int)te;
+        const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
+        const size_t fixed = smem_bytes(R, 0, b.has_rest);
+        const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
+        b.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
+        const size_t smem = smem_bytes(R, b.nstage, b.has_rest);
+        const int fit = (int)((227 * 1024) / (smem + 1024));
+        const int per_sm = std::max(1, std::min(want_ctas, fit));
+        const int64_t cap = (int64_t)sm_count() * per_sm;
+        const int grid = (int)(te - tb < cap ? te - tb : cap);
+        if (R == 4) launch_r<4>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
+        else if (R == 2) launch_r<2>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
+        else launch_r<1>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
+        HDCG_LAUNCH_CHECK("spmv_tma_kernel");
+    };
+    if (split) {
+        rest_rows(tile_begin, tile_end, st);
+        a.has_rest = 0;
+        a.init_y = 1;
+    }
+    tma(a, tile_begin, tile_end, env_ctas > 0 ? env_ctas : 3, st);
     return true;
 }
 

@@ -329,9 +329,17 @@ def test_config3_quasi_diagonal(port):
         m = H.to_mhdc(A, 0.6, bl)
         ref = port.to_mhdc(rp, col, val, 0.6, bl)
         assert_mhdc_equal(m, ref, bl)
+        want = port.spmv_mhdc(ref, x, 0)
         y = H.spmv_mhdc(m, x)
-        assert y.tobytes() == port.spmv_mhdc(ref, x, 0).tobytes()
+        assert y.tobytes() == want.tobytes()
         assert_within_tol(y, yc, rp, col, val, x)
+        try:  # every remainder mode at scale
+            for mode in (H.REST_GLOBAL, H.REST_SPLIT, H.REST_STAGED):
+                H.set_kernel_policy(H.POLICY_TMA, mode)
+                for _ in range(3):
+                    assert H.spmv_mhdc(m, x).tobytes() == want.tobytes(), (bl, mode)
+        finally:
+            H.set_kernel_policy(H.POLICY_AUTO)
         m.free()
     h = H.to_hdc(A, 0.6)
     refh = port.to_hdc(rp, col, val, 0.6)
@@ -497,7 +505,7 @@ def test_kernel_paths_bitwise_identical(port, shape):
     x = synth.x_vector(n, 7)
     xd = torch.from_numpy(x).cuda()
     try:
-        for bl in (256, 300, 512, 1000, 1024, 4096, 4097, 2 * n):
+        for bl in (128, 256, 300, 512, 1000, 1024, 4096, 4097, 2 * n):
             m = H.to_mhdc(A, 0.6, bl)
             ref = port.spmv_mhdc(port.to_mhdc(rp, col, val, 0.6, bl), x)
             outs = []
@@ -559,9 +567,10 @@ def test_reference_acceptance_through_gpu_shim():
 
 @pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT, H.REST_STAGED])
 def test_remainder_paths(port, rest_mode):
-    """The TMA kernel's three ways of summing the CSR remainder (consumers load it from
+    """The TMA kernel's ways of summing the CSR remainder (consumers load it from
     global memory; a separate rest_kernel sums it into y first; the producer stages it
-    through the TMA ring) must all be bitwise equal to the oracle, sparse and heavy."""
+    through the TMA ring)
+    must all be bitwise equal to the oracle, sparse and heavy."""
     H.set_kernel_policy(H.POLICY_TMA, rest_mode)
     try:
         _remainder_cases(port)
