@@ -175,6 +175,7 @@ void matrix_release(Matrix* m) {
     cudaFree(m->rest_val);
     cudaFree(m->dx);
     cudaFree(m->dy);
+    cudaFree(m->norm_scratch);
     for (cudaStream_t s : m->pipe)
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : m->pipe_events)

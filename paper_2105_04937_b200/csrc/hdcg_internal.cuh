@@ -64,6 +64,10 @@ struct Matrix {
     std::vector<int64_t> chunk_x_hi;    // x entries [0, chunk_x_hi[c]) chunk c reads (global)
     std::vector<int64_t> x_pieces;      // H2D pieces of x: [x_pieces[p], x_pieces[p+1])
     int64_t device_bytes = 0;
+    // per-warp partial sums of the TMA kernel's fused norm (lazily sized, reused;
+    // norm-fused SpMVs on one matrix are stream-ordered by their callers)
+    mutable double* norm_scratch = nullptr;
+    mutable int64_t norm_scratch_n = 0;
 };
 
 void matrix_release(Matrix* m);

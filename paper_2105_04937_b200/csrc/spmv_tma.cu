@@ -22,8 +22,9 @@
 //     hit L2; a warp-uniform whole-tile range test keeps per-row checks off the
 //     common path; ring bookkeeping is a (stage, phase) pair, no divisions;
 //   * y is stored once per tile (streaming store); the optional fused per-tile
-//     sum of squares has the same fixed reduction order as spmv.cu, with one
-//     consumer barrier per tile (double-buffered warp partials).
+//     sum of squares has the same fixed reduction order as spmv.cu: each warp
+//     writes its partial to a global scratch (no consumer barrier), and
+//     tile_reduce_kernel adds a tile's 8 partials in warp order afterwards.
 // Used for even bl >= 256 (all BASELINE M-HDC configurations, HDC with even n)
 // and for small blocks that tile evenly (bl in {128, 256, 512} with R = 4: a
 // tile = G = 1024/bl whole blocks; ring stage j then carries segment j of each of the G blocks,
@@ -81,7 +82,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS) : "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// The lines the consumers read at the start of a tile (the block's offsets, the
+// remainder row pointers at warp boundaries), pulled into L2 by the producer when
+// it starts the tile's copies -- one or more tiles before the consumers get there.
+__device__ __forceinline__ void prefetch_range_l2(const int32_t* base, int64_t first, int64_t last) {
+    const uintptr_t a = (uintptr_t)(base + first) & ~uintptr_t(127), e = (uintptr_t)(base + last);
+    for (uintptr_t q = a; q < e; q += 128) prefetch_l2((const void*)q);
+}
 
 struct TmaArgs {
     const int32_t* dia_ptr;
@@ -93,7 +103,7 @@ struct TmaArgs {
     const double* x;  // x_local
     double* y;
     const double* x_scale;
-    double* tile_sumsq;
+    double* warp_sumsq;  // NORM: [n_tiles * CONSUMER_WARPS] per-warp sums of y_i^2
     int64_t n_rows, n_cols, row0, bl;
     int tiles_per_block;  // > 0: a tile is a part of one block
     int blocks_per_tile;  // > 0: a tile is G whole blocks (bl < TILE, bl % (32 R) == 0)
@@ -104,6 +114,7 @@ struct TmaArgs {
     int init_y;       // remainder sums already in y (rest_kernel ran first)
     int rest_staged;  // the producer stages the remainder through the ring
     int y_vec_ok;
+    int prefetch;  // producer prefetches the consumers' tile-start lines into L2
 };
 
 struct Geo {
@@ -131,15 +142,13 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
 
 // has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest) {
-    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
-                             2 * CONSUMER_WARPS) +
+    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + (has_rest ? CONSUMER_WARPS * WPASS : 0)) +
            sizeof(uint64_t) * (2 * nstage);
 }
 
 struct Smem {
     double* ring;     // nstage * TILE
     double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
-    double* wsum;     // 2 * CONSUMER_WARPS
     uint64_t* full;
     uint64_t* empty;
 };
@@ -148,8 +157,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
     Smem s;
     s.ring = reinterpret_cast<double*>(base);
     s.scratch = s.ring + (size_t)nstage * CONSUMERS * R;
-    s.wsum = s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0);
-    s.full = reinterpret_cast<uint64_t*>(s.wsum + 2 * CONSUMER_WARPS);
+    s.full = reinterpret_cast<uint64_t*>(s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0));
     s.empty = s.full + nstage;
     return s;
 }
@@ -350,6 +358,15 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R, MB>(a, tile);
             if (g.lo >= g.hi) continue;
+            if (a.prefetch) {
+                if constexpr (REST == 1 || REST == 3) {
+#pragma unroll
+                    for (int w = 0; w <= CONSUMER_WARPS; ++w)
+                        prefetch_l2(a.rest_rp + min(g.lo + (int64_t)w * 32 * R, g.hi));
+                }
+                const int64_t bl_last = MB ? min((int64_t)g.b + a.blocks_per_tile, a.n_blocks) : (int64_t)g.b + 1;
+                prefetch_range_l2(a.dia_off, __ldg(a.dia_ptr + g.b), __ldg(a.dia_ptr + bl_last));
+            }
             if constexpr (REST == 3) {
                 constexpr int ES = rest_stage_entries<R>();
                 const int e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
@@ -426,7 +443,6 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     // -------------------------------- consumers --------------------------------
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
-    uint32_t par = 0;
     int cs = 0;             // ring stage of the next slice to consume
     uint32_t cphase = 0;    // parity of that stage's current use
     const int t0 = R * threadIdx.x;  // local row of this thread's first row
@@ -434,7 +450,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R, MB>(a, tile);
         if (g.lo >= g.hi) {
-            if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
+            if (NORM && lane == 0) a.warp_sumsq[(int64_t)tile * CONSUMER_WARPS + warp] = 0.0;
             continue;
         }
         const int rows = (int)(g.hi - g.lo);
@@ -561,18 +577,24 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                 if (t0 + r < rows) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
-            double* ws = S.wsum + par * CONSUMER_WARPS;
-            if (lane == 0) ws[warp] = s;
-            consumer_sync();
-            if (threadIdx.x == 0) {
-                double t = 0.0;
-#pragma unroll
-                for (int w = 0; w < CONSUMER_WARPS; ++w) t = __dadd_rn(t, ws[w]);
-                a.tile_sumsq[tile] = t;
-            }
-            par ^= 1;  // the next tile writes the other buffer; its barrier orders this read
+            // warp partial -> global scratch; tile_reduce_kernel adds the 8 of a
+            // tile in warp order afterwards (no consumer barrier per tile)
+            if (lane == 0) a.warp_sumsq[(int64_t)tile * CONSUMER_WARPS + warp] = s;
         }
     }
+}
+
+// tile_sumsq[t] = ((0 + w_0) + w_1) + ... + w_7: the warp partials of tile t in
+// warp order, the same fixed order as spmv_kernel's per-tile sum
+__global__ void tile_reduce_kernel(const double* __restrict__ warp_sumsq, double* __restrict__ tile_sumsq,
+                                   int64_t n) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double* p = warp_sumsq + t * CONSUMER_WARPS;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < CONSUMER_WARPS; ++w) s = __dadd_rn(s, p[w]);
+    tile_sumsq[t] = s;
 }
 
 template <int R, bool SCALE, bool NORM, int REST, bool MB>
@@ -647,7 +669,18 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.x = x_local;
     a.y = y;
     a.x_scale = x_scale;
-    a.tile_sumsq = tile_sumsq;
+    a.warp_sumsq = nullptr;
+    if (tile_sumsq) {  // per-matrix scratch for the warp partials, indexed by global tile
+        const int64_t need = tiling_of(m).n_tiles * CONSUMER_WARPS;
+        if (m.norm_scratch_n < need) {
+            if (m.norm_scratch) HDCG_CUDA(cudaFree(m.norm_scratch));
+            m.norm_scratch = nullptr;
+            m.norm_scratch_n = 0;
+            HDCG_CUDA(cudaMalloc(&m.norm_scratch, sizeof(double) * need));
+            m.norm_scratch_n = need;
+        }
+        a.warp_sumsq = m.norm_scratch;
+    }
     a.n_rows = m.n_rows;
     a.n_cols = m.n_cols;
     a.row0 = m.row0;
@@ -661,6 +694,13 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.init_y = 0;
     a.rest_staged = 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;
+    {  // HDCG_TMA_PREFETCH: A/B knob (read per call).  Default: on for multi-block
+       // tiles only -- there every tile starts on fresh block pointers and offsets
+       // (+0.5-1.5 points at bl = 256/512), while for tiles inside large blocks it
+       // cost 4-8 points at config 4 (profiles/r01_v11_prefetch_ab.log)
+        const char* e = getenv("HDCG_TMA_PREFETCH");
+        a.prefetch = e ? atoi(e) : (t.blocks_per_tile > 0 ? 1 : 0);
+    }
     // Remainder mode (hdcg_set_kernel_policy / HDCG_REST_MODE override the default):
     // 2 summed first by rest_kernel -- the default for remainder-heavy matrices (>= 1
     // entry per 4 rows); 1 loaded from global memory by the consumers -- the default
@@ -705,6 +745,12 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         else if (R == 2) launch_r<2>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
         else launch_r<1>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
         HDCG_LAUNCH_CHECK("spmv_tma_kernel");
+        if (tile_sumsq) {
+            const int64_t n = te - tb;
+            tile_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(b.warp_sumsq + tb * CONSUMER_WARPS,
+                                                                        tile_sumsq + tb, n);
+            HDCG_LAUNCH_CHECK("tile_reduce_kernel");
+        }
     };
     if (split) {
         rest_rows(tile_begin, tile_end, st);

@@ -172,13 +172,14 @@ class CudaSlab:
         self.blocks_per_tile = matrix.info.blocks_per_tile
         self.n_blocks = matrix.n_blocks
         self.launches = 0
+        self._per_spmv = len(H.spmv_kernels(matrix.info, scale=True, norm=True))
         self._out = None
 
     def spmv(self, x_buf, y_buf, b0, b1, scale, tiles):
         st = torch.cuda.current_stream().cuda_stream
         self.H.spmv_slab(self.m, x_buf.data_ptr() + 8 * self.halo, y_buf.data_ptr() + 8 * self.halo,
                          b0, b1, scale.data_ptr(), tiles.data_ptr(), st)
-        self.launches += 1
+        self.launches += self._per_spmv
 
     def tree(self, tiles):
         if self._out is None:

@@ -475,6 +475,23 @@ def gen_laplacian7(nx, ny, nz, z0, z1, rp_ptr, col_ptr, val_ptr, stream=0):
     return nnz.value
 
 
+def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
+    """The kernels one SpMV call launches for a matrix under the default policy
+    (mirrors spmv.cu::tiling_of and spmv_tma.cu::spmv_tma_launch)."""
+    r = info.tile_rows // 256
+    b = lambda v: str(v).lower()  # noqa: E731
+    inside = info.bl >= info.tile_rows  # tiles inside one block, else whole blocks per tile
+    mb = not inside and r == 4 and info.bl % 128 == 0
+    if not ((info.bl % 2 == 0 and info.bl >= 256 and inside) or mb):
+        return [f"hdcg::spmv_kernel<{r},{b(scale)},{b(norm)}>"]
+    rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
+    ks = ["hdcg::rest_kernel"] if rest == 2 else []
+    ks.append(f"hdcg::spmv_tma_kernel<{r},{b(scale)},{b(norm)},{rest},{b(mb)}>")
+    if norm:
+        ks.append("hdcg::tile_reduce_kernel")
+    return ks
+
+
 def init(device: int = 0):
     check(lib().hdcg_init(device))
 
