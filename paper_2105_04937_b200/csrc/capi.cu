@@ -113,6 +113,12 @@ T* upload(const T* host, int64_t count, cudaStream_t st) {
     return d;
 }
 
+double* upload_seg(const double* host, int64_t count, cudaStream_t st) {
+    double* d = alloc_seg(count, st);
+    if (count > 0) HDCG_CUDA(cudaMemcpyAsync(d, host, sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    return d;
+}
+
 void validate_mhdc_host(int64_t n, int64_t bl, const int32_t* dia_ptr, int64_t n_seg,
                         const int32_t* offs, const int32_t* rest_rp, int64_t nnz_rest,
                         const int32_t* rest_col) {
@@ -353,7 +359,7 @@ hdcg_status hdcg_upload_mhdc(int64_t n, int64_t bl, const int32_t* dia_ptr, int6
             m->nnz_rest = nnz_rest;
             m->dia_ptr = upload(dia_ptr, m->n_blocks + 1, st);
             m->dia_off = upload(dia_offsets, n_seg, st);
-            m->seg = upload(segments, n_seg * bl, st);
+            m->seg = upload_seg(segments, n_seg * bl, st);
             m->rest_rp = upload(rest_row_ptr, n + 1, st);
             alloc_rest(m, nnz_rest, st);
             if (nnz_rest > 0) {
@@ -417,7 +423,7 @@ hdcg_status hdcg_upload_hdc(int64_t n, int64_t n_diag, const int32_t* offsets, c
             std::vector<int32_t> dp = {0, (int32_t)m->n_seg};
             m->dia_ptr = upload(dp.data(), m->n_blocks + 1, st);
             m->dia_off = upload(offsets, m->n_seg, st);
-            m->seg = upload(lanes, m->n_seg * m->bl, st);
+            m->seg = upload_seg(lanes, m->n_seg * m->bl, st);
             m->rest_rp = upload(rest_row_ptr, n + 1, st);
             alloc_rest(m, nnz_rest, st);
             if (nnz_rest > 0) {

@@ -643,7 +643,7 @@ static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selec
     alloc_rest(m, m->nnz_rest, st);
     if (sel.n_seg > 0 && (int64_t)sel.n_seg * bl > (int64_t)1 << 40)
         fail(HDCG_ERR_OUT_OF_MEMORY, "segments too large");
-    m->seg = dev_alloc<double>(sel.n_seg * bl, st);
+    m->seg = alloc_seg(sel.n_seg * bl, st);
     const int64_t total = n_blocks * bl;
     if (total > 0) {
         fill_kernel<RP><<<grid_cap(ceil_div(total, 256)), 256, 0, st>>>(

@@ -170,6 +170,16 @@ inline void alloc_rest(Matrix* m, int64_t nnz, cudaStream_t st) {
     HDCG_CUDA(cudaMemsetAsync(m->rest_val + nnz, 0, sizeof(double) * REST_PAD, st));
 }
 
+// Segment arrays carry SEG_PAD zeroed doubles past the end: for odd bl the TMA
+// kernel moves 16-byte aligned windows that can start one slot early and end one
+// slot late.
+constexpr int64_t SEG_PAD = 2;
+inline double* alloc_seg(int64_t count, cudaStream_t st) {
+    double* p = dev_alloc<double>(count + SEG_PAD, st);
+    HDCG_CUDA(cudaMemsetAsync(p + count, 0, sizeof(double) * SEG_PAD, st));
+    return p;
+}
+
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t n_blocks_of(int64_t n, int64_t bl) { return n == 0 ? 0 : ceil_div(n, bl); }
 

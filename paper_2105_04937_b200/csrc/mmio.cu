@@ -4,9 +4,11 @@
 // CooMatrix normalisation (formats.cpp:19-43) and CsrMatrix::from_coo
 // (formats.cpp:69-88), the step in front of the converters for real inputs:
 //
-//   host   : the file is read once and its entry lines parsed by all host
-//            threads (std::from_chars: correctly rounded like the reference's
-//            `iss >> v`), chunk results concatenated in file order; the banner,
+//   host   : the file is read once (fread) and cut at line boundaries into one
+//            piece per host thread, each piece's lines parsed into (row*n+col)
+//            keys and values by its thread (std::from_chars: correctly rounded
+//            like the reference's `iss >> v`), pieces copied to the device in
+//            file order; the banner,
 //            size line, entry count, bounds, trailing tokens / content and the
 //            symmetric / skew-symmetric mirroring follow io.cpp exactly, with
 //            the same messages (runtime_error -> HDCG_ERR_IO);
@@ -79,20 +81,22 @@ bool parse_num(Line t, T* v) {
 enum Field { REAL, INTEGER, PATTERN };
 enum Symmetry { GENERAL, SYMMETRIC, SKEW };
 
-struct Parsed {
-    std::vector<int32_t> r, c;
-    std::vector<double> v;
-    std::string err;  // first error in this chunk (file order)
-    int64_t lines = 0;
-};
-
 }  // namespace
 
 // Parse + normalise; fills a device CSR (int32 row_ptr / col, f64 values).
 void read_matrix_market(const char* path, Matrix* m) {
-    std::ifstream f(path, std::ios::binary);
-    if (!f) fail(HDCG_ERR_IO, std::string("cannot open '") + path + "' for reading");
-    std::string buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    std::string buf;
+    {
+        FILE* fp = std::fopen(path, "rb");
+        if (!fp) fail(HDCG_ERR_IO, std::string("cannot open '") + path + "' for reading");
+        std::fseek(fp, 0, SEEK_END);
+        const long size = std::ftell(fp);
+        std::fseek(fp, 0, SEEK_SET);
+        buf.resize(size > 0 ? (size_t)size : 0);
+        const size_t got = buf.empty() ? 0 : std::fread(&buf[0], 1, buf.size(), fp);
+        std::fclose(fp);
+        if (got != buf.size()) fail(HDCG_ERR_IO, std::string("cannot read '") + path + "'");
+    }
     const char* p = buf.data();
     const char* end = p + buf.size();
     auto next_nonblank = [&](const char*& q, Line* line) {
@@ -146,59 +150,71 @@ void read_matrix_market(const char* path, Matrix* m) {
                      ", only square matrices are supported");
         if (rows > std::numeric_limits<int32_t>::max()) bad_file("dimension exceeds index range");
     }
+    const int64_t n = rows;
 
-    // entry lines: split the rest of the file at line boundaries, parse in parallel
-    std::vector<Line> lines;
-    lines.reserve((size_t)declared + 1);
-    {
-        const char* q = p;
-        Line l;
-        while ((int64_t)lines.size() < declared + 1 && next_nonblank(q, &l)) lines.push_back(l);
-    }
-    // entries the reference would read before it could notice a count problem
-    const int64_t avail = std::min<int64_t>((int64_t)lines.size(), declared);
+    // Entry lines: the rest of the file is cut at line boundaries into one piece
+    // per host thread; each thread counts its non-blank lines and parses them into
+    // (row*n + col) keys and values (mirrored entries right after their source, as
+    // io.cpp pushes them), keeping its first error and that line's local index.
+    // Afterwards the pieces are ordered by file position: the first error on a
+    // line the reference would read (global index < declared) is reported, then
+    // the entry-count checks -- the reference's messages and precedence.
     const unsigned hw = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
-    const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(hw, avail / 4096 + 1));
-    std::vector<Parsed> parts((size_t)chunks);
+    const int64_t body = end - p;
+    const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(hw, body / (1 << 20) + 1));
+    std::vector<const char*> cut((size_t)chunks + 1);
+    cut[0] = p;
+    cut[(size_t)chunks] = end;
+    for (int64_t ci = 1; ci < chunks; ++ci) {
+        const char* q = p + body * ci / chunks;
+        const char* e = (const char*)memchr(q, '\n', end - q);
+        cut[(size_t)ci] = std::max(cut[(size_t)ci - 1], e ? e + 1 : end);
+    }
+    struct Piece {
+        std::vector<int64_t> key;
+        std::vector<double> val;
+        std::string err;
+        int64_t err_line = -1;  // local index of the line with err
+        int64_t lines = 0;      // non-blank lines in the piece
+    };
+    std::vector<Piece> parts((size_t)chunks);
     auto work = [&](int64_t ci) {
-        Parsed& P = parts[(size_t)ci];
-        const int64_t a = avail * ci / chunks, b = avail * (ci + 1) / chunks;
-        P.r.reserve((size_t)(b - a) * (sym == GENERAL ? 1 : 2));
+        Piece& P = parts[(size_t)ci];
+        const char* q = cut[(size_t)ci];
+        const char* qe = cut[(size_t)ci + 1];
+        P.key.reserve((size_t)((qe - q) / 12 + 16) * (sym == GENERAL ? 1 : 2));
+        P.val.reserve(P.key.capacity());
         Line t[4];
-        for (int64_t k = a; k < b; ++k) {
-            const Line L = lines[(size_t)k];
-            const int n = tokens(L.b, L.e, t, 4);
+        while (q < qe) {
+            const char* e = (const char*)memchr(q, '\n', qe - q);
+            if (!e) e = qe;
+            const Line L{q, e};
+            q = e < qe ? e + 1 : qe;
+            if (is_blank(L.b, L.e)) continue;
+            const int64_t idx = P.lines++;
+            if (P.err_line >= 0) continue;  // keep counting lines only
+            const int nt = tokens(L.b, L.e, t, 4);
             long long i = 0, j = 0;
             double v = 1.0;
-            if (n < 2 || !parse_num(t[0], &i) || !parse_num(t[1], &j)) {
-                P.err = "malformed entry line '" + str(L) + "'";
-                return;
+            std::string err;
+            if (nt < 2 || !parse_num(t[0], &i) || !parse_num(t[1], &j))
+                err = "malformed entry line '" + str(L) + "'";
+            else if (field != PATTERN && (nt < 3 || !parse_num(t[2], &v)))
+                err = "missing value on entry line '" + str(L) + "'";
+            else if (nt > (field == PATTERN ? 2 : 3))
+                err = "trailing tokens on entry line '" + str(L) + "'";
+            else if (i < 1 || i > rows || j < 1 || j > cols)
+                err = "entry (" + std::to_string(i) + ", " + std::to_string(j) + ") outside declared size";
+            if (!err.empty()) {
+                P.err = err;
+                P.err_line = idx;
+                continue;
             }
-            if (field != PATTERN && (n < 3 || !parse_num(t[2], &v))) {
-                P.err = "missing value on entry line '" + str(L) + "'";
-                return;
-            }
-            if (n > (field == PATTERN ? 2 : 3)) {
-                P.err = "trailing tokens on entry line '" + str(L) + "'";
-                return;
-            }
-            if (i < 1 || i > rows || j < 1 || j > cols) {
-                P.err = "entry (" + std::to_string(i) + ", " + std::to_string(j) + ") outside declared size";
-                return;
-            }
-            P.r.push_back((int32_t)(i - 1));
-            P.c.push_back((int32_t)(j - 1));
-            P.v.push_back(v);
-            if (i != j) {
-                if (sym == SYMMETRIC) {
-                    P.r.push_back((int32_t)(j - 1));
-                    P.c.push_back((int32_t)(i - 1));
-                    P.v.push_back(v);
-                } else if (sym == SKEW) {
-                    P.r.push_back((int32_t)(j - 1));
-                    P.c.push_back((int32_t)(i - 1));
-                    P.v.push_back(-v);
-                }
+            P.key.push_back((int64_t)(i - 1) * n + (j - 1));
+            P.val.push_back(v);
+            if (i != j && sym != GENERAL) {
+                P.key.push_back((int64_t)(j - 1) * n + (i - 1));
+                P.val.push_back(sym == SKEW ? -v : v);
             }
         }
     };
@@ -208,17 +224,19 @@ void read_matrix_market(const char* path, Matrix* m) {
         work(0);
         for (auto& t : th) t.join();
     }
-    for (const Parsed& P : parts)
-        if (!P.err.empty()) bad_file(P.err);  // the first chunk (in file order) with an error
-    if ((int64_t)lines.size() < declared)
-        bad_file("expected " + std::to_string(declared) + " entries, got " + std::to_string(lines.size()));
-    if ((int64_t)lines.size() > declared) bad_file("trailing content after " + std::to_string(declared) + " entries");
+    int64_t n_lines = 0;
+    for (const Piece& P : parts) {
+        if (P.err_line >= 0 && n_lines + P.err_line < declared) bad_file(P.err);
+        n_lines += P.lines;
+    }
+    if (n_lines < declared)
+        bad_file("expected " + std::to_string(declared) + " entries, got " + std::to_string(n_lines));
+    if (n_lines > declared) bad_file("trailing content after " + std::to_string(declared) + " entries");
 
     int64_t total = 0;
-    for (const Parsed& P : parts) total += (int64_t)P.r.size();
+    for (const Piece& P : parts) total += (int64_t)P.key.size();
     if (total > std::numeric_limits<int32_t>::max())
         fail(HDCG_ERR_OVERFLOW, "CsrMatrix::from_coo: entry count exceeds index range");
-    const int64_t n = rows;
 
     // ---- device: stable sort by (row, col), in-order duplicate sums, CSR ----
     cudaStream_t st = nullptr;
@@ -227,17 +245,14 @@ void read_matrix_market(const char* path, Matrix* m) {
     double* vals = dev_alloc<double>(total, st);
     double* svals = dev_alloc<double>(total, st);
     {
-        std::vector<int64_t> hk((size_t)total);
-        std::vector<double> hv((size_t)total);
-        size_t w = 0;
-        for (const Parsed& P : parts)
-            for (size_t k = 0; k < P.r.size(); ++k, ++w) {
-                hk[w] = (int64_t)P.r[k] * n + P.c[k];
-                hv[w] = P.v[k];
+        int64_t w = 0;
+        for (const Piece& P : parts) {
+            const int64_t k = (int64_t)P.key.size();
+            if (k > 0) {
+                HDCG_CUDA(cudaMemcpyAsync(keys + w, P.key.data(), sizeof(int64_t) * k, cudaMemcpyHostToDevice, st));
+                HDCG_CUDA(cudaMemcpyAsync(vals + w, P.val.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
             }
-        if (total > 0) {
-            HDCG_CUDA(cudaMemcpyAsync(keys, hk.data(), sizeof(int64_t) * total, cudaMemcpyHostToDevice, st));
-            HDCG_CUDA(cudaMemcpyAsync(vals, hv.data(), sizeof(double) * total, cudaMemcpyHostToDevice, st));
+            w += k;
         }
         HDCG_CUDA(cudaStreamSynchronize(st));
     }

@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                 if (kk < k1) {
                     const int64_t o = __ldg(a.dia_off + kk);
                     const double* sp = seg_base + (int64_t)kk * a.bl;
-                    if (R >= 2) {
+                    // 16-byte loads unless the slice starts on an odd slot (odd bl, odd
+                    // segment index: l is a multiple of R)
+                    if (R >= 2 && !(kk & a.bl & 1)) {
 #pragma unroll
                         for (int h = 0; h < R / 2; ++h) {
                             const double2 t = __ldcs(reinterpret_cast<const double2*>(sp) + h);
@@ -147,7 +149,8 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                             v[u][2 * h + 1] = t.y;
                         }
                     } else {
-                        v[u][0] = __ldcs(sp);
+#pragma unroll
+                        for (int r = 0; r < R; ++r) v[u][r] = __ldcs(sp + r);
                     }
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
@@ -200,20 +203,22 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 
 // One tiling for both kernels (spmv_kernel and spmv_tma_kernel), so per-tile
 // partial sums and block-range alignment do not depend on which one runs:
-//   <= 8 segments per block (stencil-like) and bl % 4 == 0, >= 1024, or
-//   bl in {128, 256, 512}: 4 rows/thread, 1024-row tiles, ceil(bl/1024) tiles
-//                         per block (or 1024/bl whole blocks per tile)
-//   other even bl >= 512 : 2 rows/thread, 512-row tiles
-//   even bl in [256,512): 1 row/thread, 256-row tiles, 2 tiles per block
-//   even bl < 256      : 2 rows/thread, 512/bl whole blocks per tile
-//   odd bl             : 1 row/thread, 256-row tiles (or 256/bl blocks per tile)
+//   <= 8 segments per block (stencil-like) and bl >= 1024, or bl in {128, 256,
+//   512}: 4 rows/thread, 1024-row tiles, ceil(bl/1024) tiles per block (or
+//                         1024/bl whole blocks per tile)
+//   other bl >= 512      : 2 rows/thread, 512-row tiles
+//   bl in [256,512)      : 1 row/thread, 256-row tiles, 2 tiles per block
+//   even bl < 256        : 2 rows/thread, 512/bl whole blocks per tile
+//   odd bl < 256         : 1 row/thread, 256/bl whole blocks per tile
+// (odd bl: a slice of segment k starts on an odd slot when k is odd, so both
+// kernels fall back to 8-byte segment loads / y stores there)
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
     const bool even = m.bl % 2 == 0;
     const int64_t t4 = 4 * SPMV_THREADS;
-    if (m.bl % 4 == 0 && m.max_seg_per_block <= 8 && (m.bl >= t4 || (m.bl >= 128 && t4 % m.bl == 0)))
+    if (m.max_seg_per_block <= 8 && (m.bl >= t4 || (m.bl >= 128 && m.bl % 4 == 0 && t4 % m.bl == 0)))
         t.rows_per_thread = 4;
-    else if (even && (m.bl >= 2 * SPMV_THREADS || m.bl < SPMV_THREADS)) t.rows_per_thread = 2;
+    else if (m.bl >= 2 * SPMV_THREADS || (even && m.bl < SPMV_THREADS)) t.rows_per_thread = 2;
     else t.rows_per_thread = 1;
     t.tile_rows = (int64_t)SPMV_THREADS * t.rows_per_thread;
     if (m.bl >= t.tile_rows) {
@@ -300,7 +305,7 @@ void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_
     a.tile_rows = t.tile_rows;
     a.tile_begin = tile_begin;
     a.has_rest = m.nnz_rest > 0;
-    a.y_vec_ok = ((uintptr_t)y % 16) == 0;
+    a.y_vec_ok = ((uintptr_t)y % 16) == 0 && m.bl % 2 == 0;  // odd bl: tiles may start on odd rows
     const bool scale = x_scale != nullptr, norm = tile_sumsq != nullptr;
     if (t.rows_per_thread == 4) launch_r<4>(a, n_tiles, scale, norm, st);
     else if (t.rows_per_thread == 2) launch_r<2>(a, n_tiles, scale, norm, st);

@@ -25,7 +25,8 @@
 //     sum of squares has the same fixed reduction order as spmv.cu: each warp
 //     writes its partial to a global scratch (no consumer barrier), and
 //     tile_reduce_kernel adds a tile's 8 partials in warp order afterwards.
-// Used for even bl >= 256 (all BASELINE M-HDC configurations, HDC with even n)
+// Used for bl >= 256 (all BASELINE M-HDC configurations, HDC; odd bl with one
+// row per thread and slices copied from one slot early when they start odd)
 // and for small blocks that tile evenly (bl in {128, 256, 512} with R = 4: a
 // tile = G = 1024/bl whole blocks; ring stage j then carries segment j of each of the G blocks,
 // each warp's rows lie in one block); other shapes take the general kernel in
@@ -140,14 +141,18 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     return g;
 }
 
+// Doubles per ring stage: a tile's slice + 2 -- with odd bl a slice can start on
+// an odd slot; the 16-byte aligned copy then starts one slot early.
+__host__ __device__ constexpr int ring_stride(int R) { return CONSUMERS * R + 2; }
+
 // has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest) {
-    return sizeof(double) * ((size_t)nstage * CONSUMERS * R + (has_rest ? CONSUMER_WARPS * WPASS : 0)) +
+    return sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0)) +
            sizeof(uint64_t) * (2 * nstage);
 }
 
 struct Smem {
-    double* ring;     // nstage * TILE
+    double* ring;     // nstage * ring_stride(R)
     double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
     uint64_t* full;
     uint64_t* empty;
@@ -156,7 +161,7 @@ struct Smem {
 __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int has_rest) {
     Smem s;
     s.ring = reinterpret_cast<double*>(base);
-    s.scratch = s.ring + (size_t)nstage * CONSUMERS * R;
+    s.scratch = s.ring + (size_t)nstage * ring_stride(R);
     s.full = reinterpret_cast<uint64_t*>(s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0));
     s.empty = s.full + nstage;
     return s;
@@ -284,7 +289,7 @@ __device__ __forceinline__ void staged_rest(const TmaArgs& a, const Smem& S, dou
     for (int c = e_lo & ~3; c < c_end; c += ES) {
         const int n = min(ES, c_end - c);
         mbar_wait(&S.full[cs], cphase);
-        const double* sval = S.ring + cs * TILE;
+        const double* sval = S.ring + cs * ring_stride(R);
         const int32_t* scol = reinterpret_cast<const int32_t*>(sval + ES);
         const int q0 = max(we0, c), q1 = min(we1, c + n);
         for (int p = q0; p < q1; p += PASS) {
@@ -328,11 +333,18 @@ __device__ __forceinline__ void staged_rest(const TmaArgs& a, const Smem& S, dou
 // REST: 0 no remainder, 1 remainder summed here from global memory (fused),
 // 2 remainder sums already in y (rest_kernel ran first), 3 remainder staged
 // through the ring by the producer (staged_rest)
-// MB: multi-block tiles (a.blocks_per_tile > 0), instantiated for R = 4 only
-template <int R, bool SCALE, bool NORM, int REST, bool MB>
+// LAY: tile layout.  0 tiles inside one block, even bl; 1 multi-block tiles
+// (a.blocks_per_tile > 0, R = 4 only); 2 tiles inside one block, odd bl
+// (slices of odd segments start on an odd slot).
+template <int R, bool SCALE, bool NORM, int REST, int LAY>
 __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
+    constexpr bool MB = LAY == 1;
+    constexpr bool ODD = LAY == 2;
     constexpr int TILE = CONSUMERS * R;
-    constexpr int XG = XGROUP_ROWS / R;  // x registers per thread stay at XGROUP_ROWS doubles
+    constexpr int STRIDE = ring_stride(R);
+    // x registers per thread stay at XGROUP_ROWS doubles (half that for the odd
+    // layout, whose shifted stage reads need the registers)
+    constexpr int XG = (ODD ? XGROUP_ROWS / 2 : XGROUP_ROWS) / R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
     const Smem S = carve(smem_raw, R, NS, a.has_rest);
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                         const uint32_t n = (uint32_t)min(ES, c_end - c);
                         if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
                         mbar_expect_tx(&S.full[ps], n * 12u);
-                        double* dst = S.ring + ps * TILE;
+                        double* dst = S.ring + ps * STRIDE;
                         bulk_g2s(dst, a.rest_val + c, n * 8u, &S.full[ps], policy);
                         bulk_g2s(dst + ES, a.rest_col + c, n * 4u, &S.full[ps], policy);
                         if (++ps == NS) {
@@ -413,7 +425,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
                     for (int q = 0; q < GMAX; ++q)
                         if (j < cnt[q])
-                            bulk_g2s(S.ring + ps * TILE + q * a.bl, a.seg + (int64_t)(kst[q] + j) * a.bl, pb[q],
+                            bulk_g2s(S.ring + ps * STRIDE + q * a.bl, a.seg + (int64_t)(kst[q] + j) * a.bl, pb[q],
                                      &S.full[ps], policy);
                     if (++ps == NS) {
                         ps = 0;
@@ -424,12 +436,18 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                 continue;
             }
             const int k0 = __ldg(a.dia_ptr + g.b), k1 = __ldg(a.dia_ptr + g.b + 1);
-            const uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
-            const double* src = a.seg + (int64_t)k0 * a.bl + (g.lo - g.b0);
+            const int64_t off0 = g.lo - g.b0;
+            uint32_t bytes = (uint32_t)(((g.hi - g.lo + 1) & ~int64_t(1)) * 8);
+            const double* src = a.seg + (int64_t)k0 * a.bl + off0;
             for (int k = k0; k < k1; ++k, src += a.bl) {
+                // odd bl: the slice starts on an odd slot (k odd, or an odd tile start
+                // for R = 1); copy from one slot earlier (16-byte aligned), consumers
+                // read at +1
+                const int sh = ODD ? ((k & (int)a.bl) ^ (int)off0) & 1 : 0;
+                if (ODD) bytes = (uint32_t)(((g.hi - g.lo + sh + 1) & ~int64_t(1)) * 8);
                 if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);  // previous use released
                 mbar_expect_tx(&S.full[ps], bytes);
-                bulk_g2s(S.ring + ps * TILE, src, bytes, &S.full[ps], policy);
+                bulk_g2s(S.ring + ps * STRIDE, src - sh, bytes, &S.full[ps], policy);
                 if (++ps == NS) {
                     ps = 0;
                     pphase ^= 1u;
@@ -523,9 +541,28 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                 for (int u = 0; u < XG; ++u) {
                     if (u < ng) {
                         mbar_wait(&S.full[cs], cphase);
-                        const double* st = S.ring + cs * TILE + t0;
+                        const double* st = S.ring + cs * STRIDE + t0;
+                        // odd bl: the slice may sit one slot in (see the producer)
+                        // (bl odd: k*bl has k's parity; tile starts are even for R >= 2)
+                        const int sh = !ODD ? 0
+                                            : R >= 2 ? (kb0 + kg + u) & 1 : ((kb0 + kg + u) ^ (int)(g.lo - g.b0)) & 1;
                         double v[R];
-                        if (R >= 2) {
+                        if (ODD && R >= 2) {
+                            // the slice may start one slot in (sh): this thread's values
+                            // are then e[1..R] of its aligned R-group -- 16-byte loads of
+                            // e[0..R-1] (conflict-free), e[R] from the next lane's e[0]
+                            double e[R];
+#pragma unroll
+                            for (int h = 0; h < R / 2; ++h) {
+                                const double2 t = reinterpret_cast<const double2*>(st)[h];
+                                e[2 * h] = t.x;
+                                e[2 * h + 1] = t.y;
+                            }
+                            double last = __shfl_down_sync(0xffffffffu, e[0], 1);
+                            if (lane == 31 && sh) last = st[R];
+#pragma unroll
+                            for (int r = 0; r < R; ++r) v[r] = sh ? (r + 1 < R ? e[r + 1] : last) : e[r];
+                        } else if (R >= 2) {
 #pragma unroll
                             for (int h = 0; h < R / 2; ++h) {
                                 const double2 t = reinterpret_cast<const double2*>(st)[h];
@@ -533,7 +570,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                                 v[2 * h + 1] = t.y;
                             }
                         } else {
-                            v[0] = st[0];
+                            v[0] = st[sh];
                         }
                         if (u < nv) {
 #pragma unroll
@@ -560,7 +597,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         }
 
         if (t0 < rows) {
-            if (R >= 2 && a.y_vec_ok && t0 + R - 1 < rows) {
+            if (R >= 2 && (ODD ? ((uintptr_t)(a.y + i0) & 15) == 0 : a.y_vec_ok) && t0 + R - 1 < rows) {
 #pragma unroll
                 for (int h = 0; h < R / 2; ++h)
                     __stcs(reinterpret_cast<double2*>(a.y + i0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));
@@ -597,9 +634,9 @@ __global__ void tile_reduce_kernel(const double* __restrict__ warp_sumsq, double
     tile_sumsq[t] = s;
 }
 
-template <int R, bool SCALE, bool NORM, int REST, bool MB>
+template <int R, bool SCALE, bool NORM, int REST, int LAY>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
-    auto k = spmv_tma_kernel<R, SCALE, NORM, REST, MB>;
+    auto k = spmv_tma_kernel<R, SCALE, NORM, REST, LAY>;
     static bool configured = false;  // per instantiation
     if (!configured) {
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -608,31 +645,32 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     k<<<grid, THREADS, smem, st>>>(a);
 }
 
-template <int R, int REST, bool MB>
+template <int R, int REST, int LAY>
 void launch_rr(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if (scale) {
-        if (norm) launch_one<R, true, true, REST, MB>(a, grid, smem, st);
-        else launch_one<R, true, false, REST, MB>(a, grid, smem, st);
+        if (norm) launch_one<R, true, true, REST, LAY>(a, grid, smem, st);
+        else launch_one<R, true, false, REST, LAY>(a, grid, smem, st);
     } else {
-        if (norm) launch_one<R, false, true, REST, MB>(a, grid, smem, st);
-        else launch_one<R, false, false, REST, MB>(a, grid, smem, st);
+        if (norm) launch_one<R, false, true, REST, LAY>(a, grid, smem, st);
+        else launch_one<R, false, false, REST, LAY>(a, grid, smem, st);
     }
 }
 
-template <int R, bool MB>
+template <int R, int LAY>
 void launch_m(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
-    if (a.init_y) launch_rr<R, 2, MB>(a, grid, smem, scale, norm, st);
-    else if (a.has_rest && a.rest_staged) launch_rr<R, 3, MB>(a, grid, smem, scale, norm, st);
-    else if (a.has_rest) launch_rr<R, 1, MB>(a, grid, smem, scale, norm, st);
-    else launch_rr<R, 0, MB>(a, grid, smem, scale, norm, st);
+    if (a.init_y) launch_rr<R, 2, LAY>(a, grid, smem, scale, norm, st);
+    else if (a.has_rest && a.rest_staged) launch_rr<R, 3, LAY>(a, grid, smem, scale, norm, st);
+    else if (a.has_rest) launch_rr<R, 1, LAY>(a, grid, smem, scale, norm, st);
+    else launch_rr<R, 0, LAY>(a, grid, smem, scale, norm, st);
 }
 
 template <int R>
 void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if constexpr (R == 4) {
-        if (a.blocks_per_tile > 0) return launch_m<4, true>(a, grid, smem, scale, norm, st);
+        if (a.blocks_per_tile > 0) return launch_m<4, 1>(a, grid, smem, scale, norm, st);
     }
-    launch_m<R, false>(a, grid, smem, scale, norm, st);
+    if (a.bl % 2) launch_m<R, 2>(a, grid, smem, scale, norm, st);
+    else launch_m<R, 0>(a, grid, smem, scale, norm, st);
 }
 
 int sm_count() {
@@ -650,7 +688,6 @@ int sm_count() {
 
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st) {
-    if (m.bl % 2 != 0 || m.bl < CONSUMERS) return false;
     if (m.n_seg > 0 && ((uintptr_t)m.seg % 16) != 0) return false;
     if (m.nnz_rest > 0 && (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0)) return false;
     const Tiling t = tiling_of(m);
@@ -693,7 +730,7 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.has_rest = m.nnz_rest > 0;
     a.init_y = 0;
     a.rest_staged = 0;
-    a.y_vec_ok = ((uintptr_t)y % 16) == 0;
+    a.y_vec_ok = ((uintptr_t)y % 16) == 0;  // (odd bl: tiles may start on odd rows, tested per thread)
     {  // HDCG_TMA_PREFETCH: A/B knob (read per call).  Default: on for multi-block
        // tiles only -- there every tile starts on fresh block pointers and offsets
        // (+0.5-1.5 points at bl = 256/512), while for tiles inside large blocks it

@@ -482,11 +482,12 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     b = lambda v: str(v).lower()  # noqa: E731
     inside = info.bl >= info.tile_rows  # tiles inside one block, else whole blocks per tile
     mb = not inside and r == 4 and info.bl % 128 == 0
-    if not ((info.bl % 2 == 0 and info.bl >= 256 and inside) or mb):
+    if not ((info.bl >= 256 and inside) or mb):
         return [f"hdcg::spmv_kernel<{r},{b(scale)},{b(norm)}>"]
     rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
     ks = ["hdcg::rest_kernel"] if rest == 2 else []
-    ks.append(f"hdcg::spmv_tma_kernel<{r},{b(scale)},{b(norm)},{rest},{b(mb)}>")
+    lay = 1 if mb else (2 if info.bl % 2 else 0)  # tile layout: inside one block / multi-block / odd bl
+    ks.append(f"hdcg::spmv_tma_kernel<{r},{b(scale)},{b(norm)},{rest},{lay}>")
     if norm:
         ks.append("hdcg::tile_reduce_kernel")
     return ks

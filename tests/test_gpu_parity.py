@@ -505,7 +505,7 @@ def test_kernel_paths_bitwise_identical(port, shape):
     x = synth.x_vector(n, 7)
     xd = torch.from_numpy(x).cuda()
     try:
-        for bl in (128, 256, 300, 512, 1000, 1024, 4096, 4097, 2 * n):
+        for bl in (128, 256, 257, 300, 512, 1000, 1001, 1024, 4096, 4097, 2 * n):
             m = H.to_mhdc(A, 0.6, bl)
             ref = port.spmv_mhdc(port.to_mhdc(rp, col, val, 0.6, bl), x)
             outs = []
@@ -521,7 +521,7 @@ def test_kernel_paths_bitwise_identical(port, shape):
                 assert y2.tobytes() == ref.tobytes(), (shape, bl, pol)
             assert outs[0][0].tobytes() == outs[1][0].tobytes(), (shape, bl)
             assert outs[0][1].tobytes() == outs[1][1].tobytes(), (shape, bl)
-            if bl % 2 == 0 and bl >= 256:
+            if "tma" in H.spmv_kernels(m.info)[-1]:  # odd bl >= 256 and bl = 128 included
                 H.set_kernel_policy(H.POLICY_TMA)
                 assert H.spmv_mhdc(m, x).tobytes() == ref.tobytes()
             m.free()
@@ -595,7 +595,7 @@ def _remainder_cases(port):
         vals = np.concatenate([val, rng.uniform(-1, 1, extra)])
         rp2, col2, val2 = synth.coo_to_csr(n, rows, cols, vals)
         x = synth.x_vector(n, 3)
-        for bl in (1024, 4096, 512, 384):
+        for bl in (1024, 4096, 512, 384, 1023):
             ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
             m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
             assert_mhdc_equal(m, ref, (extra, bl))
