@@ -200,6 +200,31 @@ hdcg_status hdcg_spmv_slab(hdcg_matrix m, const double* x_local, double* y, int6
                            int64_t block_end, const double* x_scale, double* tile_sumsq,
                            void* stream);
 
+/* Row-slab SpMV that also delivers the slab's halo rows to its neighbours
+ * through peer memory (NVLink P2P stores from the SpMV epilogue -- the
+ * exchange overlaps the computation tile by tile, no separate collective):
+ * as hdcg_spmv_slab, and additionally rows i < halo are stored to
+ * peer_lo[i] (the lower neighbour's upper halo) and rows i >= n_rows - halo to
+ * peer_hi[i - (n_rows - halo)] (the upper neighbour's lower halo), followed by
+ * a system-scope fence.  peer_lo / peer_hi may be NULL (no such neighbour) and
+ * are device pointers valid on this device (hdcg_peer_open).  The caller orders
+ * the neighbour's reads after this kernel (the power iteration's per-step norm
+ * all-gather does).  There is no reference counterpart: the reference has no
+ * distributed path. */
+hdcg_status hdcg_spmv_slab_halo(hdcg_matrix m, const double* x_local, double* y, int64_t block_begin,
+                                int64_t block_end, const double* x_scale, double* tile_sumsq, double* peer_lo,
+                                double* peer_hi, int64_t halo, void* stream);
+
+/* Peer memory for the halo exchange: hdcg_peer_alloc returns a device buffer
+ * on the current device and its 64-byte inter-process handle; another process
+ * (another GPU of the node, or the same GPU) maps it with hdcg_peer_open
+ * (peer access enabled lazily) and unmaps it with hdcg_peer_close;
+ * hdcg_peer_free releases the owner's buffer. */
+hdcg_status hdcg_peer_alloc(int64_t bytes, void** ptr, unsigned char handle[64]);
+hdcg_status hdcg_peer_open(const unsigned char handle[64], void** ptr);
+hdcg_status hdcg_peer_close(void* ptr);
+hdcg_status hdcg_peer_free(void* ptr);
+
 /* Kernel selection (process-wide): policy & 3 = 0 automatic (the TMA-fed
  * persistent kernel for even bl >= 256, the general kernel otherwise), 1 general
  * kernel only, 2 TMA kernel only (ineligible shapes then fail with

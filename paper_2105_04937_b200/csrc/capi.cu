@@ -181,7 +181,6 @@ void matrix_release(Matrix* m) {
     cudaFree(m->rest_val);
     cudaFree(m->dx);
     cudaFree(m->dy);
-    cudaFree(m->norm_scratch);
     for (cudaStream_t s : m->pipe)
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : m->pipe_events)
@@ -549,6 +548,56 @@ hdcg_status hdcg_spmv_slab(hdcg_matrix h, const double* x_local, double* y, int6
         const Matrix* m = unwrap(h);
         spmv_launch(*m, x_local, y, block_begin, block_end, x_scale, tile_sumsq, (cudaStream_t)stream);
     });
+}
+
+hdcg_status hdcg_spmv_slab_halo(hdcg_matrix h, const double* x_local, double* y, int64_t block_begin,
+                                int64_t block_end, const double* x_scale, double* tile_sumsq, double* peer_lo,
+                                double* peer_hi, int64_t halo, void* stream) {
+    return guard([&] {
+        const Matrix* m = unwrap(h);
+        if (halo < 0 || halo > m->n_rows) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: halo outside the slab");
+        PeerOut p;
+        p.lo = peer_lo;
+        p.hi = peer_hi;
+        p.halo = halo;
+        spmv_launch(*m, x_local, y, block_begin, block_end, x_scale, tile_sumsq, (cudaStream_t)stream, p);
+    });
+}
+
+hdcg_status hdcg_peer_alloc(int64_t bytes, void** ptr, unsigned char handle[64]) {
+    return guard([&] {
+        if (!ptr || !handle || bytes < 1) fail(HDCG_ERR_INVALID_ARGUMENT, "peer_alloc: bad arguments");
+        use_device();
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        void* p = nullptr;
+        HDCG_CUDA(cudaMalloc(&p, (size_t)bytes));
+        cudaIpcMemHandle_t hd;
+        const cudaError_t e = cudaIpcGetMemHandle(&hd, p);
+        if (e != cudaSuccess) {
+            cudaFree(p);
+            HDCG_CUDA(e);
+        }
+        std::memcpy(handle, &hd, 64);
+        *ptr = p;
+    });
+}
+
+hdcg_status hdcg_peer_open(const unsigned char handle[64], void** ptr) {
+    return guard([&] {
+        if (!ptr || !handle) fail(HDCG_ERR_INVALID_ARGUMENT, "peer_open: bad arguments");
+        use_device();
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, handle, 64);
+        HDCG_CUDA(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+hdcg_status hdcg_peer_close(void* ptr) {
+    return guard([&] { HDCG_CUDA(cudaIpcCloseMemHandle(ptr)); });
+}
+
+hdcg_status hdcg_peer_free(void* ptr) {
+    return guard([&] { HDCG_CUDA(cudaFree(ptr)); });
 }
 
 hdcg_status hdcg_spmv_host(hdcg_matrix h, const double* x, double* y) {

@@ -64,10 +64,6 @@ struct Matrix {
     std::vector<int64_t> chunk_x_hi;    // x entries [0, chunk_x_hi[c]) chunk c reads (global)
     std::vector<int64_t> x_pieces;      // H2D pieces of x: [x_pieces[p], x_pieces[p+1])
     int64_t device_bytes = 0;
-    // per-warp partial sums of the TMA kernel's fused norm (lazily sized, reused;
-    // norm-fused SpMVs on one matrix are stream-ordered by their callers)
-    mutable double* norm_scratch = nullptr;
-    mutable int64_t norm_scratch_n = 0;
 };
 
 void matrix_release(Matrix* m);
@@ -102,15 +98,26 @@ __host__ __device__ inline void tile_rows(int64_t t, int64_t tiles_per_block, in
     }
 }
 
+// Peer-memory halo: rows i < halo of the slab are also stored to lo[i] (the lower
+// neighbour's upper halo), rows i >= n_rows - halo to hi[i - (n_rows - halo)]
+// (the upper neighbour's lower halo), from the kernel's epilogue, then fenced at
+// system scope.  Either pointer may be null.
+struct PeerOut {
+    double* lo = nullptr;
+    double* hi = nullptr;
+    int64_t halo = 0;
+};
+
 // Launch over a tile range (both kernels); spmv_launch maps block ranges onto it.
 void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
-                       const double* x_scale, double* tile_sumsq, cudaStream_t st);
+                       const double* x_scale, double* tile_sumsq, cudaStream_t st, const PeerOut& peer = PeerOut());
 
 void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin,
-                 int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st);
+                 int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st,
+                 const PeerOut& peer = PeerOut());
 // the TMA-fed persistent kernel (spmv_tma.cu); false when the shape is not eligible
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
-                     const double* x_scale, double* tile_sumsq, cudaStream_t st);
+                     const double* x_scale, double* tile_sumsq, cudaStream_t st, const PeerOut& peer);
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
 extern int g_rest_mode;      // TMA kernel remainder mode (hdcg_set_kernel_policy), 0 default
 // Matrix Market ingestion (mmio.cu)

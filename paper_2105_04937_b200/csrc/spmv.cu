@@ -57,6 +57,9 @@ struct SpmvArgs {
     int64_t tile_begin;
     int has_rest;
     int y_vec_ok;
+    double* peer_lo;  // PeerOut
+    double* peer_hi;
+    int64_t halo;
 };
 
 template <int R, bool SCALE, bool NORM>
@@ -181,6 +184,16 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
             for (int r = 0; r < R; ++r)
                 if (i0 + r < hi) __stcs(a.y + i0 + r, acc[r]);
         }
+        if (a.peer_lo || a.peer_hi) {  // halo rows also to the neighbours (peer memory)
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int64_t i = i0 + r;
+                if (i >= hi) continue;
+                if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc[r];
+                if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc[r];
+            }
+            __threadfence_system();
+        }
     }
 
     if (NORM) {
@@ -250,7 +263,8 @@ static void launch_r(const SpmvArgs& a, int64_t n_tiles, bool scale, bool norm, 
 }
 
 void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t block_begin,
-                 int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st) {
+                 int64_t block_end, const double* x_scale, double* tile_sumsq, cudaStream_t st,
+                 const PeerOut& peer) {
     if (block_begin < 0 || block_end > m.n_blocks || block_begin > block_end)
         fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: block range outside the matrix");
     const Tiling t = tiling_of(m);
@@ -265,11 +279,11 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
         tile_begin = block_begin / t.blocks_per_tile;
         tile_end = ceil_div(block_end, t.blocks_per_tile);
     }
-    spmv_launch_tiles(m, x_local, y, tile_begin, tile_end, x_scale, tile_sumsq, st);
+    spmv_launch_tiles(m, x_local, y, tile_begin, tile_end, x_scale, tile_sumsq, st, peer);
 }
 
 void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
-                       const double* x_scale, double* tile_sumsq, cudaStream_t st) {
+                       const double* x_scale, double* tile_sumsq, cudaStream_t st, const PeerOut& peer) {
     static const int env_policy = [] {  // HDCG_KERNEL_POLICY: profiling override of the default
         const char* e = getenv("HDCG_KERNEL_POLICY");
         if (e) g_kernel_policy = atoi(e);
@@ -282,7 +296,7 @@ void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_
     const int64_t n_tiles = tile_end - tile_begin;
     if (n_tiles <= 0) return;
     if (tile_end > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "spmv: too many tiles for one launch");
-    if (g_kernel_policy != 1 && spmv_tma_launch(m, x_local, y, tile_begin, tile_end, x_scale, tile_sumsq, st))
+    if (g_kernel_policy != 1 && spmv_tma_launch(m, x_local, y, tile_begin, tile_end, x_scale, tile_sumsq, st, peer))
         return;
     if (g_kernel_policy == 2) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: TMA kernel requested for an ineligible shape");
     SpmvArgs a;
@@ -306,6 +320,9 @@ void spmv_launch_tiles(const Matrix& m, const double* x_local, double* y, int64_
     a.tile_begin = tile_begin;
     a.has_rest = m.nnz_rest > 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0 && m.bl % 2 == 0;  // odd bl: tiles may start on odd rows
+    a.peer_lo = peer.lo;
+    a.peer_hi = peer.hi;
+    a.halo = peer.halo;
     const bool scale = x_scale != nullptr, norm = tile_sumsq != nullptr;
     if (t.rows_per_thread == 4) launch_r<4>(a, n_tiles, scale, norm, st);
     else if (t.rows_per_thread == 2) launch_r<2>(a, n_tiles, scale, norm, st);

@@ -22,9 +22,8 @@
 //     hit L2; a warp-uniform whole-tile range test keeps per-row checks off the
 //     common path; ring bookkeeping is a (stage, phase) pair, no divisions;
 //   * y is stored once per tile (streaming store); the optional fused per-tile
-//     sum of squares has the same fixed reduction order as spmv.cu: each warp
-//     writes its partial to a global scratch (no consumer barrier), and
-//     tile_reduce_kernel adds a tile's 8 partials in warp order afterwards.
+//     sum of squares has the same fixed reduction order as spmv.cu, with one
+//     consumer barrier per tile (double-buffered warp partials).
 // Used for bl >= 256 (all BASELINE M-HDC configurations, HDC; odd bl with one
 // row per thread and slices copied from one slot early when they start odd)
 // and for small blocks that tile evenly (bl in {128, 256, 512} with R = 4: a
@@ -83,6 +82,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -104,7 +104,7 @@ struct TmaArgs {
     const double* x;  // x_local
     double* y;
     const double* x_scale;
-    double* warp_sumsq;  // NORM: [n_tiles * CONSUMER_WARPS] per-warp sums of y_i^2
+    double* tile_sumsq;
     int64_t n_rows, n_cols, row0, bl;
     int tiles_per_block;  // > 0: a tile is a part of one block
     int blocks_per_tile;  // > 0: a tile is G whole blocks (bl < TILE, bl % (32 R) == 0)
@@ -115,6 +115,9 @@ struct TmaArgs {
     int init_y;       // remainder sums already in y (rest_kernel ran first)
     int rest_staged;  // the producer stages the remainder through the ring
     int y_vec_ok;
+    double* peer_lo;  // PeerOut: halo rows also stored to the neighbours
+    double* peer_hi;
+    int64_t halo;
     int prefetch;  // producer prefetches the consumers' tile-start lines into L2
 };
 
@@ -147,13 +150,15 @@ __host__ __device__ constexpr int ring_stride(int R) { return CONSUMERS * R + 2;
 
 // has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest) {
-    return sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0)) +
+    return sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
+                             2 * CONSUMER_WARPS) +
            sizeof(uint64_t) * (2 * nstage);
 }
 
 struct Smem {
     double* ring;     // nstage * ring_stride(R)
     double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
+    double* wsum;     // 2 * CONSUMER_WARPS (fused norm: double-buffered warp partials)
     uint64_t* full;
     uint64_t* empty;
 };
@@ -162,7 +167,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
     Smem s;
     s.ring = reinterpret_cast<double*>(base);
     s.scratch = s.ring + (size_t)nstage * ring_stride(R);
-    s.full = reinterpret_cast<uint64_t*>(s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0));
+    s.wsum = s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0);
+    s.full = reinterpret_cast<uint64_t*>(s.wsum + 2 * CONSUMER_WARPS);
     s.empty = s.full + nstage;
     return s;
 }
@@ -463,12 +469,13 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     if (SCALE) sc = *a.x_scale;
     int cs = 0;             // ring stage of the next slice to consume
     uint32_t cphase = 0;    // parity of that stage's current use
+    uint32_t par = 0;
     const int t0 = R * threadIdx.x;  // local row of this thread's first row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R, MB>(a, tile);
         if (g.lo >= g.hi) {
-            if (NORM && lane == 0) a.warp_sumsq[(int64_t)tile * CONSUMER_WARPS + warp] = 0.0;
+            if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
             continue;
         }
         const int rows = (int)(g.hi - g.lo);
@@ -606,6 +613,15 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                 for (int r = 0; r < R; ++r)
                     if (t0 + r < rows) __stcs(a.y + i0 + r, acc[r]);
             }
+            if (a.peer_lo || a.peer_hi) {  // halo rows also to the neighbours (peer memory)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int64_t i = i0 + r;
+                    if (t0 + r >= rows) continue;
+                    if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc[r];
+                    if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc[r];
+                }
+            }
         }
         if (NORM) {
             double s = 0.0;
@@ -614,24 +630,25 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                 if (t0 + r < rows) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
-            // warp partial -> global scratch; tile_reduce_kernel adds the 8 of a
-            // tile in warp order afterwards (no consumer barrier per tile)
-            if (lane == 0) a.warp_sumsq[(int64_t)tile * CONSUMER_WARPS + warp] = s;
+            // the tile's 8 warp partials in warp order, one consumer barrier per tile
+            // (double-buffered partials).  A barrier-free variant (partials to a global
+            // scratch, summed by a second kernel) measured 8% more DRAM reads at config 4
+            // -- the x lines' L2 reuse across the +-nx*ny offsets suffered -- and was
+            // dropped (profiles/r01_v14_norm_variants.log).
+            double* ws = S.wsum + par * CONSUMER_WARPS;
+            if (lane == 0) ws[warp] = s;
+            consumer_sync();
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+#pragma unroll
+                for (int w = 0; w < CONSUMER_WARPS; ++w) t = __dadd_rn(t, ws[w]);
+                a.tile_sumsq[tile] = t;
+            }
+            par ^= 1;  // the next tile writes the other buffer; its barrier orders this read
         }
     }
-}
-
-// tile_sumsq[t] = ((0 + w_0) + w_1) + ... + w_7: the warp partials of tile t in
-// warp order, the same fixed order as spmv_kernel's per-tile sum
-__global__ void tile_reduce_kernel(const double* __restrict__ warp_sumsq, double* __restrict__ tile_sumsq,
-                                   int64_t n) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const double* p = warp_sumsq + t * CONSUMER_WARPS;
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < CONSUMER_WARPS; ++w) s = __dadd_rn(s, p[w]);
-    tile_sumsq[t] = s;
+    // remote halo stores are visible system-wide before the kernel completes
+    if (a.peer_lo || a.peer_hi) __threadfence_system();
 }
 
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
@@ -687,7 +704,7 @@ int sm_count() {
 }  // namespace
 
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
-                     const double* x_scale, double* tile_sumsq, cudaStream_t st) {
+                     const double* x_scale, double* tile_sumsq, cudaStream_t st, const PeerOut& peer) {
     if (m.n_seg > 0 && ((uintptr_t)m.seg % 16) != 0) return false;
     if (m.nnz_rest > 0 && (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0)) return false;
     const Tiling t = tiling_of(m);
@@ -706,18 +723,7 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.x = x_local;
     a.y = y;
     a.x_scale = x_scale;
-    a.warp_sumsq = nullptr;
-    if (tile_sumsq) {  // per-matrix scratch for the warp partials, indexed by global tile
-        const int64_t need = tiling_of(m).n_tiles * CONSUMER_WARPS;
-        if (m.norm_scratch_n < need) {
-            if (m.norm_scratch) HDCG_CUDA(cudaFree(m.norm_scratch));
-            m.norm_scratch = nullptr;
-            m.norm_scratch_n = 0;
-            HDCG_CUDA(cudaMalloc(&m.norm_scratch, sizeof(double) * need));
-            m.norm_scratch_n = need;
-        }
-        a.warp_sumsq = m.norm_scratch;
-    }
+    a.tile_sumsq = tile_sumsq;
     a.n_rows = m.n_rows;
     a.n_cols = m.n_cols;
     a.row0 = m.row0;
@@ -731,6 +737,9 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.init_y = 0;
     a.rest_staged = 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;  // (odd bl: tiles may start on odd rows, tested per thread)
+    a.peer_lo = peer.lo;
+    a.peer_hi = peer.hi;
+    a.halo = peer.halo;
     {  // HDCG_TMA_PREFETCH: A/B knob (read per call).  Default: on for multi-block
        // tiles only -- there every tile starts on fresh block pointers and offsets
        // (+0.5-1.5 points at bl = 256/512), while for tiles inside large blocks it
@@ -782,12 +791,6 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         else if (R == 2) launch_r<2>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
         else launch_r<1>(b, grid, smem, x_scale != nullptr, tile_sumsq != nullptr, s);
         HDCG_LAUNCH_CHECK("spmv_tma_kernel");
-        if (tile_sumsq) {
-            const int64_t n = te - tb;
-            tile_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(b.warp_sumsq + tb * CONSUMER_WARPS,
-                                                                        tile_sumsq + tb, n);
-            HDCG_LAUNCH_CHECK("tile_reduce_kernel");
-        }
     };
     if (split) {
         rest_rows(tile_begin, tile_end, st);

@@ -20,8 +20,15 @@ ranks; the tree over tiles is split into per-rank subtrees (power-of-two tile
 counts per rank) so the norm is bitwise independent of it too.
 
 The compute backend is injected: CudaSlab (libhdcgpu.so, the product) or, in
-the CPU tests only, an oracle-backed stand-in.  The transport is
-torch.distributed (NCCL on GPUs, gloo in the CPU tests).
+the CPU tests only, an oracle-backed stand-in.  The halo transport is either
+  * "nccl": torch.distributed send/recv of the boundary rows (NCCL over NVLink;
+    gloo in the CPU tests), overlapped with the interior blocks, or
+  * "p2p": PeerHalo -- the boundary SpMV itself stores its halo rows into the
+    neighbours' buffers through peer memory (CUDA IPC mappings, NVLink P2P
+    stores from the kernel epilogue), so the exchange overlaps the computation
+    tile by tile and no collective is launched for it.  The per-step norm
+    all-gather orders those stores before the neighbours' next reads (and
+    their reads before the next overwrite: x/y are double-buffered).
 """
 from __future__ import annotations
 
@@ -103,6 +110,69 @@ class HaloExchange:
             q.wait()
 
 
+class PeerHalo:
+    """Peer-memory halo delivery for a rank whose two slab buffers are
+    hdcgpu.PeerBuffer objects (layout [H | rows | H]).  Maps the neighbours'
+    buffers: lo[i] = the lower neighbour's buffer i at its upper halo (where
+    this rank's first H rows go), hi[i] = the upper neighbour's buffer i at its
+    lower halo (this rank's last H rows)."""
+
+    def __init__(self, plan: SlabPlan, rank: int, peer_bufs):
+        from . import hdcgpu as H
+        self.H, self.plan, self.rank = H, plan, rank
+        handles = [b.handle for b in peer_bufs]
+        allh = [None] * plan.world
+        dist.all_gather_object(allh, handles)
+        self.mapped, self.lo, self.hi = [], [0, 0], [0, 0]
+        if rank > 0:
+            for i in range(2):
+                base = H.peer_open(allh[rank - 1][i])
+                self.mapped.append(base)
+                self.lo[i] = base + 8 * (plan.halo + plan.rows[rank - 1])
+        if rank < plan.world - 1:
+            for i in range(2):
+                base = H.peer_open(allh[rank + 1][i])
+                self.mapped.append(base)
+                self.hi[i] = base
+
+    def close(self):
+        for p in self.mapped:
+            self.H.peer_close(p)
+        self.mapped = []
+
+
+def halo_checksums(plan: SlabPlan, rank: int, buf: torch.Tensor) -> torch.Tensor:
+    """int64 sums of the bit patterns of [first H rows, last H rows, lower halo,
+    upper halo] of a slab buffer (exact: integer arithmetic)."""
+    Hh, rows = plan.halo, plan.rows[rank]
+    v = buf.view(torch.int64)
+    return torch.stack([v[Hh:2 * Hh].sum(), v[rows:rows + Hh].sum(), v[0:Hh].sum(),
+                        v[Hh + rows:2 * Hh + rows].sum()])
+
+
+def verify_halos(plan: SlabPlan, rank: int, buf: torch.Tensor) -> bool:
+    """True when every rank's halos of `buf` hold exactly its neighbours' boundary rows."""
+    cs = halo_checksums(plan, rank, buf)
+    allc = [torch.zeros_like(cs) for _ in range(plan.world)]
+    dist.all_gather(allc, cs)
+    ok = True
+    for r in range(plan.world):
+        if r > 0 and int(allc[r][2]) != int(allc[r - 1][1]):
+            ok = False
+        if r < plan.world - 1 and int(allc[r][3]) != int(allc[r + 1][0]):
+            ok = False
+    return ok
+
+
+def _all_gather_roots(out: torch.Tensor, local: torch.Tensor):
+    if out.is_cuda and dist.get_backend() == "gloo":  # CPU tests on one GPU: stage through the host
+        parts = [torch.zeros(1, dtype=out.dtype) for _ in range(out.numel())]
+        dist.all_gather(parts, local.cpu())
+        out.copy_(torch.cat(parts))
+    else:
+        dist.all_gather_into_tensor(out, local)
+
+
 def pairwise_tree(vals: torch.Tensor) -> torch.Tensor:
     """Host-side twin of hdcg_tree_sum for tiny vectors (rank roots): pads to a
     power of two with +0.0 and adds adjacent pairs level by level."""
@@ -121,14 +191,21 @@ class SlabPowerIteration:
     """Drives the config-4 power iteration over one rank's slab.
 
     compute must provide: n_tiles, blocks_per_tile, n_blocks,
-      spmv(x_buf, y_buf, b0, b1, scale, tiles)   -- y_buf[H:H+rows] <- A_slab (scale * x_buf)
+      spmv(x_buf, y_buf, b0, b1, scale, tiles[, peer_lo, peer_hi])
+                                                 -- y_buf[H:H+rows] <- A_slab (scale * x_buf)
       tree(tiles) -> tensor([sum, 1/sqrt(sum)])  -- deterministic pairwise tree
+    peer: a PeerHalo (x0_buf and y_buf are then views of its two PeerBuffers,
+    in that order) -- the boundary SpMVs deliver the halos; otherwise NCCL/gloo
+    send/recv does.
     """
 
-    def __init__(self, plan: SlabPlan, rank: int, compute, x0_buf: torch.Tensor, comm=True):
+    def __init__(self, plan: SlabPlan, rank: int, compute, x0_buf: torch.Tensor, comm=True,
+                 y_buf: torch.Tensor | None = None, peer: PeerHalo | None = None):
         self.plan, self.rank, self.c = plan, rank, compute
-        self.bufs = [x0_buf, torch.empty_like(x0_buf)]
+        self.bufs = [x0_buf, torch.empty_like(x0_buf) if y_buf is None else y_buf]
         self.bufs[1].zero_()
+        self.peer = peer
+        self.yi = 1  # index (into the original pair) of the buffer y goes to this step
         dev = x0_buf.device
         self.scale = torch.ones(1, dtype=torch.float64, device=dev)
         self.tiles = torch.zeros(compute.n_tiles, dtype=torch.float64, device=dev)
@@ -145,6 +222,18 @@ class SlabPowerIteration:
             red = self.c.tree(self.tiles)
             self.scale.copy_(red[1:2])
             self.red = red
+        elif self.peer is not None:
+            # boundary blocks store their halo rows straight into the neighbours' y
+            # buffers (same parity on every rank); the all-gather below orders them
+            lo, hi = self.peer.lo[self.yi], self.peer.hi[self.yi]
+            for b0, b1 in self.parts:
+                self.c.spmv(x, y, b0, b1, self.scale, self.tiles, lo, hi)
+            if self.interior[1] > self.interior[0]:
+                self.c.spmv(x, y, self.interior[0], self.interior[1], self.scale, self.tiles)
+            local = self.c.tree(self.tiles)
+            _all_gather_roots(self.roots, local[0:1].contiguous())
+            self.red = self.c.tree(self.roots)
+            self.scale.copy_(self.red[1:2])
         else:
             for b0, b1 in self.parts:
                 self.c.spmv(x, y, b0, b1, self.scale, self.tiles)
@@ -153,12 +242,13 @@ class SlabPowerIteration:
                 self.c.spmv(x, y, self.interior[0], self.interior[1], self.scale, self.tiles)
             HaloExchange.wait(reqs)
             local = self.c.tree(self.tiles)
-            dist.all_gather_into_tensor(self.roots, local[0:1].contiguous())
+            _all_gather_roots(self.roots, local[0:1].contiguous())
             # the top of the tree over the rank roots: the same padded pairwise tree,
             # one launch on the device (stream-ordered after the all-gather)
             self.red = self.c.tree(self.roots)
             self.scale.copy_(self.red[1:2])
         self.bufs.reverse()
+        self.yi ^= 1
         return self.red
 
 
@@ -175,10 +265,14 @@ class CudaSlab:
         self._per_spmv = len(H.spmv_kernels(matrix.info, scale=True, norm=True))
         self._out = None
 
-    def spmv(self, x_buf, y_buf, b0, b1, scale, tiles):
+    def spmv(self, x_buf, y_buf, b0, b1, scale, tiles, peer_lo=0, peer_hi=0):
         st = torch.cuda.current_stream().cuda_stream
-        self.H.spmv_slab(self.m, x_buf.data_ptr() + 8 * self.halo, y_buf.data_ptr() + 8 * self.halo,
-                         b0, b1, scale.data_ptr(), tiles.data_ptr(), st)
+        if peer_lo or peer_hi:
+            self.H.spmv_slab_halo(self.m, x_buf.data_ptr() + 8 * self.halo, y_buf.data_ptr() + 8 * self.halo,
+                                  b0, b1, scale.data_ptr(), tiles.data_ptr(), peer_lo, peer_hi, self.halo, st)
+        else:
+            self.H.spmv_slab(self.m, x_buf.data_ptr() + 8 * self.halo, y_buf.data_ptr() + 8 * self.halo,
+                             b0, b1, scale.data_ptr(), tiles.data_ptr(), st)
         self.launches += self._per_spmv
 
     def tree(self, tiles):

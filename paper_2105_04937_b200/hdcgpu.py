@@ -32,7 +32,8 @@ from typing import NamedTuple
 import numpy as np
 
 # HDCG_LIBRARY: another in-tree build of the same library (same-box A/B of kernel versions)
-LIB_PATH = os.environ.get("HDCG_LIBRARY") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhdcgpu.so")
+_DEFAULT_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhdcgpu.so")
+LIB_PATH = os.environ.get("HDCG_LIBRARY") or _DEFAULT_LIB
 
 HDCG_INPUT_DEVICE = 1
 HDCG_VALIDATE = 2
@@ -46,7 +47,8 @@ EXPORTS = (
     "hdcg_build_csr", "hdcg_upload_mhdc", "hdcg_upload_hdc", "hdcg_free", "hdcg_get_info",
     "hdcg_export", "hdcg_rates", "hdcg_census", "hdcg_spmv", "hdcg_spmv_host", "hdcg_spmv_slab",
     "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7", "hdcg_set_kernel_policy",
-    "hdcg_membench", "hdcg_analyze", "hdcg_read_matrix_market",
+    "hdcg_membench", "hdcg_analyze", "hdcg_read_matrix_market", "hdcg_spmv_slab_halo",
+    "hdcg_peer_alloc", "hdcg_peer_open", "hdcg_peer_close", "hdcg_peer_free",
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
@@ -111,6 +113,11 @@ def lib():
         "hdcg_spmv": [vp, vp, vp, vp],
         "hdcg_spmv_host": [vp, vp, vp],
         "hdcg_spmv_slab": [vp, vp, vp, i64, i64, vp, vp, vp],
+        "hdcg_spmv_slab_halo": [vp, vp, vp, i64, i64, vp, vp, vp, vp, i64, vp],
+        "hdcg_peer_alloc": [i64, C.POINTER(vp), C.c_char_p],
+        "hdcg_peer_open": [C.c_char_p, C.POINTER(vp)],
+        "hdcg_peer_close": [vp],
+        "hdcg_peer_free": [vp],
         "hdcg_tree_sum": [vp, i64, vp, vp],
         "hdcg_set_kernel_policy": [C.c_int],
         "hdcg_membench": [i64, C.c_int, C.c_int, C.c_int, C.POINTER(f64), C.POINTER(f64), vp],
@@ -120,6 +127,8 @@ def lib():
         "hdcg_gen_laplacian7": [i64, i64, i64, i64, i64, vp, vp, vp, C.POINTER(i64), vp],
     }
     for name, args in sig.items():
+        if LIB_PATH != _DEFAULT_LIB and not hasattr(L, name):
+            continue  # an older build loaded for an A/B (HDCG_LIBRARY): bind what it has
         f = getattr(L, name)
         f.argtypes = args
         f.restype = C.c_int
@@ -445,6 +454,47 @@ def spmv_slab(m: DeviceMatrix, x_local_ptr: int, y_ptr: int, block_begin: int, b
                                x_scale_ptr or None, tile_sumsq_ptr or None, stream or None))
 
 
+def spmv_slab_halo(m: DeviceMatrix, x_local_ptr: int, y_ptr: int, block_begin: int, block_end: int,
+                   x_scale_ptr: int, tile_sumsq_ptr: int, peer_lo_ptr: int, peer_hi_ptr: int, halo: int,
+                   stream: int = 0):
+    """spmv_slab that also stores the slab's first/last `halo` rows into the
+    neighbours' halo buffers (peer memory) from the kernel epilogue."""
+    check(lib().hdcg_spmv_slab_halo(m.handle, x_local_ptr, y_ptr, block_begin, block_end, x_scale_ptr or None,
+                                    tile_sumsq_ptr or None, peer_lo_ptr or None, peer_hi_ptr or None, halo,
+                                    stream or None))
+
+
+class PeerBuffer:
+    """A float64 device buffer another process can map (CUDA IPC through
+    hdcg_peer_alloc); exposes __cuda_array_interface__, so torch.as_tensor(buf,
+    device="cuda") views it without a copy."""
+
+    def __init__(self, count: int):
+        self.count = count
+        p = C.c_void_p()
+        h = C.create_string_buffer(64)
+        check(lib().hdcg_peer_alloc(8 * max(1, count), C.byref(p), h))
+        self.ptr, self.handle = p.value, h.raw
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+
+    def free(self):
+        if self.ptr:
+            check(lib().hdcg_peer_free(self.ptr))
+            self.ptr = None
+
+
+def peer_open(handle: bytes) -> int:
+    """Map a PeerBuffer of another process; returns the device address."""
+    p = C.c_void_p()
+    check(lib().hdcg_peer_open(handle, C.byref(p)))
+    return p.value
+
+
+def peer_close(ptr: int):
+    check(lib().hdcg_peer_close(ptr))
+
+
 def tree_sum(vals_ptr: int, count: int, out_ptr: int, stream: int = 0):
     check(lib().hdcg_tree_sum(vals_ptr or None, count, out_ptr, stream or None))
 
@@ -488,8 +538,6 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     ks = ["hdcg::rest_kernel"] if rest == 2 else []
     lay = 1 if mb else (2 if info.bl % 2 else 0)  # tile layout: inside one block / multi-block / odd bl
     ks.append(f"hdcg::spmv_tma_kernel<{r},{b(scale)},{b(norm)},{rest},{lay}>")
-    if norm:
-        ks.append("hdcg::tile_reduce_kernel")
     return ks
 
 

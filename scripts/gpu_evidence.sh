@@ -1,16 +1,26 @@
 #!/bin/bash
-# Evidence for profiles/: the default bench line (N=1, with CPU baseline), its ncu
-# launch list, and one ncu --set full capture of the SpMV kernel of the same command.
+# Evidence for profiles/: the default bench line (N=1, with CPU baseline), the
+# reference arm, every configuration's line (c1 block-size sweep, HDC, CSR), the
+# ncu launch list of the default command and one ncu --set full capture of its
+# SpMV kernel.
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-python scripts/bw_probe.py > gpurun_out/bw.json 2>&1
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
-timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
-for w in c1 c2 c3; do timeout 600 python bench.py --no-cpu-baseline --workload $w --steps 20 --warmup 3 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; done
-timeout 600 python bench.py --no-cpu-baseline --workload c1 --format hdc --steps 20 --warmup 3 > gpurun_out/bench_c1_hdc.json 2> gpurun_out/bench_c1_hdc.err
-timeout 600 python bench.py --no-cpu-baseline --workload c3 --bl 1024 --steps 20 --warmup 3 > gpurun_out/bench_c3_bl1024.json 2> gpurun_out/bench_c3_bl1024.err
+mkdir -p gpurun_out/ev
+O=gpurun_out/ev
+python scripts/bw_probe.py > $O/bw.json 2>&1
+timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+timeout 300 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_reference.json 2> $O/bench_reference.err
+for bl in 256 512 1024 4096 16384; do
+  timeout 600 python bench.py --no-cpu-baseline --workload c1 --bl $bl --steps 20 --warmup 3 > $O/bench_c1_bl$bl.json 2> $O/bench_c1_bl$bl.err
+done
+timeout 600 python bench.py --no-cpu-baseline --workload c1 --format hdc --steps 20 --warmup 3 > $O/bench_c1_hdc.json 2> $O/bench_c1_hdc.err
+timeout 600 python bench.py --no-cpu-baseline --workload c2 --steps 20 --warmup 3 > $O/bench_c2.json 2> $O/bench_c2.err
+timeout 600 python bench.py --no-cpu-baseline --workload c3 --steps 20 --warmup 3 > $O/bench_c3.json 2> $O/bench_c3.err
+timeout 600 python bench.py --no-cpu-baseline --workload c3 --bl 1024 --steps 20 --warmup 3 > $O/bench_c3_bl1024.json 2> $O/bench_c3_bl1024.err
+for w in c1 c2 c3; do
+  timeout 600 python bench.py --workload $w --format csr --steps 20 --warmup 3 > $O/bench_${w}_csr.json 2> $O/bench_${w}_csr.err
+done
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
-timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:spmv_tma -s 3 -c 1 -o gpurun_out/prof_c4_final $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 600 $CMD > $O/plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv $CMD > $O/ncu_launch.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:spmv_tma -s 3 -c 1 -o $O/prof_c4 $CMD > $O/ncu_full.log 2>&1
 echo done

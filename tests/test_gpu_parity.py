@@ -755,3 +755,67 @@ def test_matrix_market_large_parallel_parse(tmp_path, port):
     assert np.array_equal(got.row_ptr.astype(np.int64), want[0])
     assert np.array_equal(got.col_ind, want[1])
     assert got.values.tobytes() == want[2].tobytes()
+
+
+# ---------------------------------------------------------------------------
+# peer-memory halo (the p2p transport of dist.py), two processes on one GPU
+
+def _peer_halo_worker(rank, world, port, nx, ny, nz, bl, steps, out_dir):
+    import torch.distributed as dist
+
+    from paper_2105_04937_b200.dist import CudaSlab, PeerHalo, SlabPlan, SlabPowerIteration, verify_halos
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    H.init(0)
+    n, halo = nx * ny * nz, nx * ny
+    plan = SlabPlan.make(n, bl, halo, world, unit=nx * ny)
+    row0, rows = plan.row0[rank], plan.rows[rank]
+    z0, z1 = row0 // halo, (row0 + rows) // halo
+    nnz = H.gen_laplacian7_nnz(nx, ny, nz, z0, z1)
+    d_rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+    d_col = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    d_val = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    H.gen_laplacian7(nx, ny, nz, z0, z1, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr())
+    m = H.build_mhdc_device(rows, n, row0, nnz, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr(), 0.6, bl)
+    pbufs = [H.PeerBuffer(rows + 2 * halo) for _ in range(2)]
+    xb, yb = (torch.as_tensor(b, device="cuda") for b in pbufs)
+    xb.zero_()
+    g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
+    H.gen_uniform_pm1(5, 0, g0, g1 - g0, xb.data_ptr() + 8 * (g0 - (row0 - halo)))
+    peer = PeerHalo(plan, rank, pbufs) if world > 1 else None
+    it = SlabPowerIteration(plan, rank, CudaSlab(m, halo), xb, comm=world > 1, y_buf=yb, peer=peer)
+    for _ in range(steps):
+        it.step()
+    torch.cuda.synchronize()
+    ok = verify_halos(plan, rank, it.bufs[0]) if world > 1 else True
+    np.save(os.path.join(out_dir, f"y{world}_{rank}.npy"), it.bufs[0][halo:halo + rows].cpu().numpy())
+    np.save(os.path.join(out_dir, f"red{world}_{rank}.npy"), it.red.cpu().numpy())
+    np.save(os.path.join(out_dir, f"ok{world}_{rank}.npy"), np.array([ok]))
+    dist.barrier()
+    if peer is not None:
+        peer.close()
+    dist.destroy_process_group()
+
+
+def test_peer_halo_power_iteration_two_processes(tmp_path):
+    """dist.py's p2p transport: two ranks (processes sharing this GPU through CUDA
+    IPC mappings) run the config-4 power iteration on z-slabs; the boundary SpMVs
+    store their halo rows straight into the neighbour's buffers.  y and ||y|| are
+    bitwise those of one rank, and the halos hold exactly the neighbours' rows."""
+    import socket
+
+    import torch.multiprocessing as mp
+    nx, ny, nz, bl, steps = 32, 32, 16, 256, 4
+    for world in (1, 2):
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        mp.spawn(_peer_halo_worker, args=(world, port, nx, ny, nz, bl, steps, str(tmp_path)), nprocs=world,
+                 join=True)
+    y1 = np.load(tmp_path / "y1_0.npy")
+    y2 = np.concatenate([np.load(tmp_path / f"y2_{r}.npy") for r in range(2)])
+    assert y2.tobytes() == y1.tobytes()
+    for r in range(2):
+        assert np.load(tmp_path / f"red2_{r}.npy").tobytes() == np.load(tmp_path / "red1_0.npy").tobytes()
+        assert bool(np.load(tmp_path / f"ok2_{r}.npy")[0])
