@@ -37,7 +37,7 @@ namespace hdcg {
 constexpr int SPMV_THREADS = 256;
 
 int g_kernel_policy = 0;  // 0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA only
-int g_rest_mode = 0;      // TMA kernel remainder: 0 default, 1 global loads, 2 rest_kernel first, 3 staged
+int g_rest_mode = 0;      // TMA kernel remainder: 0 default, 1 global loads, 2 rest_kernel first
 constexpr int REST_CHUNK = 1024;  // doubles of staged remainder products
 constexpr int SEG_UNROLL = 8;
 
@@ -62,7 +62,10 @@ struct SpmvArgs {
     int64_t halo;
 };
 
-template <int R, bool SCALE, bool NORM>
+// IL: interleaved rows (thread t owns tile rows t, t+256, ...) -- tiles inside
+// one block, the TMA kernel's mapping (so per-tile sums agree bitwise); otherwise
+// (whole blocks per tile) R consecutive rows per thread.
+template <int R, bool SCALE, bool NORM, bool IL>
 __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
     __shared__ double prod[REST_CHUNK];
     __shared__ double warp_sums[SPMV_THREADS / 32];
@@ -80,7 +83,10 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
         lo = tile * a.blocks_per_tile * a.bl;
         hi = min(lo + a.blocks_per_tile * a.bl, a.n_rows);
     }
-    const int64_t i0 = lo + (int64_t)R * threadIdx.x;
+    // row of this thread's r-th row
+    auto row = [&](int r) -> int64_t {
+        return IL ? lo + threadIdx.x + (int64_t)SPMV_THREADS * r : lo + (int64_t)R * threadIdx.x + r;
+    };
 
     double acc[R];
 #pragma unroll
@@ -96,7 +102,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
             int64_t kb[R], ke[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int64_t i = i0 + r;
+                const int64_t i = row(r);
                 if (i < hi) {
                     kb[r] = a.rest_rp[i];
                     ke[r] = a.rest_rp[i + 1];
@@ -123,14 +129,16 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
     }
 
     // ---- diagonal segments of this row's block, stored order ----------------
+    const int64_t i0 = row(0);
     if (i0 < hi) {
-        const int64_t b = i0 / a.bl;
+        const int64_t b = i0 / a.bl;  // all of this thread's rows are in one block
         const int64_t l = i0 - b * a.bl;
         const int k0 = __ldg(a.dia_ptr + b);
         const int k1 = __ldg(a.dia_ptr + b + 1);
         const int64_t gi = a.row0 + i0;
         const double* seg_base = a.seg + l;
         constexpr int U = R == 4 ? 4 : SEG_UNROLL;
+        constexpr int64_t RS = IL ? SPMV_THREADS : 1;  // row stride between a thread's rows
         for (int k = k0; k < k1; k += U) {
             double v[U][R];
             double xv[U][R];
@@ -142,9 +150,9 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                 if (kk < k1) {
                     const int64_t o = __ldg(a.dia_off + kk);
                     const double* sp = seg_base + (int64_t)kk * a.bl;
-                    // 16-byte loads unless the slice starts on an odd slot (odd bl, odd
-                    // segment index: l is a multiple of R)
-                    if (R >= 2 && !(kk & a.bl & 1)) {
+                    // 16-byte loads for consecutive rows unless the slice starts on an
+                    // odd slot (odd bl, odd segment index: l is a multiple of R)
+                    if (!IL && R >= 2 && !(kk & a.bl & 1)) {
 #pragma unroll
                         for (int h = 0; h < R / 2; ++h) {
                             const double2 t = __ldcs(reinterpret_cast<const double2*>(sp) + h);
@@ -153,13 +161,14 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                         }
                     } else {
 #pragma unroll
-                        for (int r = 0; r < R; ++r) v[u][r] = __ldcs(sp + r);
+                        for (int r = 0; r < R; ++r)
+                            if (i0 + RS * r < hi) v[u][r] = __ldcs(sp + RS * r);
                     }
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int64_t j = gi + r + o;
-                        const bool ok = (j >= 0) & (j < a.n_cols) & (i0 + r < hi);
-                        if (ok) xv[u][r] = __ldg(a.x + (i0 + r + o));
+                        const int64_t j = gi + RS * r + o;
+                        const bool ok = (j >= 0) & (j < a.n_cols) & (i0 + RS * r < hi);
+                        if (ok) xv[u][r] = __ldg(a.x + (i0 + RS * r + o));
                     }
                 }
             }
@@ -175,19 +184,19 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                 }
             }
         }
-        if (R >= 2 && a.y_vec_ok && i0 + R - 1 < hi) {
+        if (!IL && R >= 2 && a.y_vec_ok && i0 + R - 1 < hi) {
 #pragma unroll
             for (int h = 0; h < R / 2; ++h)
                 __stcs(reinterpret_cast<double2*>(a.y + i0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));
         } else {
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (i0 + r < hi) __stcs(a.y + i0 + r, acc[r]);
+                if (i0 + RS * r < hi) __stcs(a.y + i0 + RS * r, acc[r]);
         }
         if (a.peer_lo || a.peer_hi) {  // halo rows also to the neighbours (peer memory)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int64_t i = i0 + r;
+                const int64_t i = i0 + RS * r;
                 if (i >= hi) continue;
                 if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc[r];
                 if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc[r];
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
         double s = 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r)
-            if (i0 + r < hi) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
+            if (row(r) < hi) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
         if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = s;
@@ -248,7 +257,8 @@ Tiling tiling_of(const Matrix& m) {
 
 template <int R, bool SCALE, bool NORM>
 static void launch_t(const SpmvArgs& a, int64_t n_tiles, cudaStream_t st) {
-    spmv_kernel<R, SCALE, NORM><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
+    if (a.tiles_per_block > 0) spmv_kernel<R, SCALE, NORM, true><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
+    else spmv_kernel<R, SCALE, NORM, false><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
 }
 
 template <int R>

@@ -11,25 +11,30 @@
 //     mbarrier transaction counts, L2 evict-first (segments are read once).  The
 //     ring holds only matrix data -- the bytes that come from DRAM -- so ~70 KB
 //     per CTA (~210 KB per SM) of HBM traffic is in flight;
-//   * warps 0-7 consume in the reference's order: first the CSR remainder, each
-//     warp for its own 32*R rows (their entries are contiguous: coalesced
-//     evict-first loads, 8 independent x gathers per lane in flight, products in
-//     a per-warp scratch, per-row sequential sums; warp-synchronous), then per
-//     segment: the block's offsets were loaded once per tile by
-//     each warp (one coalesced load, broadcast with shuffles); x values are
-//     loaded for a group of XGROUP segments ahead of the stage waits through the
-//     L1/tex path, where the near offsets of a tile share lines and the far ones
-//     hit L2; a warp-uniform whole-tile range test keeps per-row checks off the
+//   * warps 0-7 consume in the reference's order: first the CSR remainder
+//     (each warp for its own rows: their entries are contiguous per 32-row run:
+//     coalesced evict-first loads, 8 independent x gathers per lane in flight,
+//     products in a per-warp scratch, per-row sequential sums; warp-synchronous),
+//     then per segment: the block's offsets were loaded once per tile by each
+//     warp (one coalesced load, broadcast with shuffles); x values are loaded for
+//     a group of XGROUP segments ahead of the stage waits through the L1/tex
+//     path, where the near offsets of a tile share lines and the far ones hit
+//     L2; a warp-uniform whole-tile range test keeps per-row checks off the
 //     common path; ring bookkeeping is a (stage, phase) pair, no divisions;
+//   * rows are interleaved over the threads (thread t: tile rows t, t+256, ...),
+//     so each x load, shared read and y store of a warp touches 32 consecutive
+//     rows -- the L1 data pipe was 90% busy with 4 consecutive rows per thread
+//     (8 wavefronts per x load, 2-way conflicted 16-byte shared reads);
+//     multi-block tiles keep consecutive rows so a warp stays in one block;
 //   * y is stored once per tile (streaming store); the optional fused per-tile
 //     sum of squares has the same fixed reduction order as spmv.cu, with one
 //     consumer barrier per tile (double-buffered warp partials).
-// Used for bl >= 256 (all BASELINE M-HDC configurations, HDC; odd bl with one
-// row per thread and slices copied from one slot early when they start odd)
-// and for small blocks that tile evenly (bl in {128, 256, 512} with R = 4: a
-// tile = G = 1024/bl whole blocks; ring stage j then carries segment j of each of the G blocks,
-// each warp's rows lie in one block); other shapes take the general kernel in
-// spmv.cu.
+// Used for bl >= 256 (all BASELINE M-HDC configurations, HDC; odd bl: slices
+// that start on an odd slot are copied from one slot early) and for small
+// blocks that tile evenly (bl in {128, 256, 512} with R = 4: a tile = G =
+// 1024/bl whole blocks; ring stage j then carries segment j of each of the G
+// blocks, each warp's rows lie in one block); other shapes take the general
+// kernel in spmv.cu.
 #include <algorithm>
 #include <cstdlib>
 
@@ -113,7 +118,6 @@ struct TmaArgs {
     int nstage;
     int has_rest;
     int init_y;       // remainder sums already in y (rest_kernel ran first)
-    int rest_staged;  // the producer stages the remainder through the ring
     int y_vec_ok;
     double* peer_lo;  // PeerOut: halo rows also stored to the neighbours
     double* peer_hi;
@@ -253,92 +257,8 @@ __global__ void __launch_bounds__(CONSUMERS, MINB) rest_kernel(const TmaArgs a, 
         if (i0 + r < hi) a.y[i0 + r] = acc[r];
 }
 
-// Remainder entries per ring stage when the producer stages them (REST == 3): a
-// stage holds TILE doubles; ES values (8 B) + ES columns (4 B), ES a multiple of 32.
-template <int R>
-__host__ __device__ constexpr int rest_stage_entries() {
-    return (CONSUMERS * R * 8 / 12) / 32 * 32;
-}
-
-// Staged remainder (REST == 3): the producer has copied the tile's remainder
-// entries [e_lo & ~3, (e_hi + 3) & ~3) into consecutive ring stages with TMA
-// (values, then columns, in each stage).  Each warp takes, stage by stage, the
-// part of its own rows' entries that lies in the stage: columns and values come
-// from shared memory, x is gathered (the only global loads left on this path,
-// PER per lane in flight), products go to the warp's scratch and each lane adds
-// its rows' products in stored order.  Every warp waits for and releases every
-// rest stage of the tile (the ring is shared).
-template <int R, bool SCALE>
-__device__ __forceinline__ void staged_rest(const TmaArgs& a, const Smem& S, double sc, int64_t lo, int64_t hi,
-                                            int e_lo, int e_hi, int warp, int lane, int& cs, uint32_t& cphase,
-                                            double (&acc)[R]) {
-    constexpr int TILE = CONSUMERS * R;
-    constexpr int ES = rest_stage_entries<R>();
-    constexpr int PER = R == 4 ? 4 : 8;
-    constexpr int PASS = 32 * PER;
-    static_assert(PASS <= WPASS, "scratch too small");
-    const int t0 = R * (warp * 32 + lane);
-    const int rows = (int)(hi - lo);
-    const int64_t i0 = lo + t0;
-    const int64_t w_lo = min(lo + (int64_t)warp * 32 * R, hi);
-    const int64_t w_hi = min(w_lo + 32 * R, hi);
-    const int we0 = __ldg(a.rest_rp + w_lo), we1 = __ldg(a.rest_rp + w_hi);
-    int kb[R], ke[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const bool ok = t0 + r < rows;
-        kb[r] = ok ? __ldg(a.rest_rp + i0 + r) : 0;
-        ke[r] = ok ? __ldg(a.rest_rp + i0 + r + 1) : 0;
-    }
-    double* scratch = S.scratch + warp * WPASS;
-    const int c_end = (e_hi + 3) & ~3;
-    for (int c = e_lo & ~3; c < c_end; c += ES) {
-        const int n = min(ES, c_end - c);
-        mbar_wait(&S.full[cs], cphase);
-        const double* sval = S.ring + cs * ring_stride(R);
-        const int32_t* scol = reinterpret_cast<const int32_t*>(sval + ES);
-        const int q0 = max(we0, c), q1 = min(we1, c + n);
-        for (int p = q0; p < q1; p += PASS) {
-            double xl[PER], vl[PER];
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                const int q = p + lane + 32 * j;
-                xl[j] = 0.0;
-                vl[j] = 0.0;
-                if (q < q1) {
-                    vl[j] = sval[q - c];
-                    xl[j] = __ldg(a.x + ((int64_t)scol[q - c] - a.row0));
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < PER; ++j) {
-                double xv = xl[j];
-                if (SCALE) xv = __dmul_rn(xv, sc);
-                scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
-            }
-            __syncwarp();
-            const int pe = min(q1, p + PASS);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int p0 = max(kb[r], p), p1 = min(ke[r], pe);
-                for (int u = p0; u < p1; ++u) acc[r] = __dadd_rn(acc[r], scratch[u - p]);
-            }
-            __syncwarp();
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[cs]);
-        if (++cs == a.nstage) {
-            cs = 0;
-            cphase ^= 1u;
-        }
-    }
-}
-
 // REST: 0 no remainder, 1 remainder summed here from global memory (fused),
-// 2 remainder sums already in y (rest_kernel ran first), 3 remainder staged
-// through the ring by the producer (staged_rest)
+// 2 remainder sums already in y (rest_kernel ran first)
 // LAY: tile layout.  0 tiles inside one block, even bl; 1 multi-block tiles
 // (a.blocks_per_tile > 0, R = 4 only); 2 tiles inside one block, odd bl
 // (slices of odd segments start on an odd slot).
@@ -348,9 +268,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     constexpr bool ODD = LAY == 2;
     constexpr int TILE = CONSUMERS * R;
     constexpr int STRIDE = ring_stride(R);
-    // x registers per thread stay at XGROUP_ROWS doubles (half that for the odd
-    // layout, whose shifted stage reads need the registers)
-    constexpr int XG = (ODD ? XGROUP_ROWS / 2 : XGROUP_ROWS) / R;
+    constexpr int XG = XGROUP_ROWS / R;  // x registers per thread stay at XGROUP_ROWS doubles
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
     const Smem S = carve(smem_raw, R, NS, a.has_rest);
@@ -377,33 +295,13 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             const Geo g = geo<R, MB>(a, tile);
             if (g.lo >= g.hi) continue;
             if (a.prefetch) {
-                if constexpr (REST == 1 || REST == 3) {
+                if constexpr (REST == 1) {
 #pragma unroll
                     for (int w = 0; w <= CONSUMER_WARPS; ++w)
                         prefetch_l2(a.rest_rp + min(g.lo + (int64_t)w * 32 * R, g.hi));
                 }
                 const int64_t bl_last = MB ? min((int64_t)g.b + a.blocks_per_tile, a.n_blocks) : (int64_t)g.b + 1;
                 prefetch_range_l2(a.dia_off, __ldg(a.dia_ptr + g.b), __ldg(a.dia_ptr + bl_last));
-            }
-            if constexpr (REST == 3) {
-                constexpr int ES = rest_stage_entries<R>();
-                const int e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
-                const int c_end = (e_hi + 3) & ~3;
-                if (e_hi > e_lo) {
-                    for (int c = e_lo & ~3; c < c_end; c += ES) {
-                        const uint32_t n = (uint32_t)min(ES, c_end - c);
-                        if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
-                        mbar_expect_tx(&S.full[ps], n * 12u);
-                        double* dst = S.ring + ps * STRIDE;
-                        bulk_g2s(dst, a.rest_val + c, n * 8u, &S.full[ps], policy);
-                        bulk_g2s(dst + ES, a.rest_col + c, n * 4u, &S.full[ps], policy);
-                        if (++ps == NS) {
-                            ps = 0;
-                            pphase ^= 1u;
-                            p_wrapped = true;
-                        }
-                    }
-                }
             }
             if constexpr (MB) {
                 // stage j = segment j of each of the tile's blocks, block q's slots at
@@ -465,12 +363,19 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     }
 
     // -------------------------------- consumers --------------------------------
+    // Row mapping: tiles inside one block (LAY 0, 2) are interleaved -- thread t
+    // owns tile rows t, t+256, ..., so every x load, shared-memory read and y store
+    // of a warp covers 32 consecutive rows (2 L1 wavefronts per 8-byte access
+    // instead of 8 with 4 consecutive rows per thread); multi-block tiles (LAY 1)
+    // keep 4 consecutive rows per thread so that a warp's rows stay in one block.
+    constexpr bool IL = !MB;
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
     int cs = 0;             // ring stage of the next slice to consume
     uint32_t cphase = 0;    // parity of that stage's current use
     uint32_t par = 0;
-    const int t0 = R * threadIdx.x;  // local row of this thread's first row
+    const int t0 = IL ? (int)threadIdx.x : R * (int)threadIdx.x;  // local row of this thread's first row
+    auto lr = [&](int r) { return IL ? t0 + CONSUMERS * r : t0 + r; };  // local row of its r-th row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R, MB>(a, tile);
@@ -479,7 +384,6 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             continue;
         }
         const int rows = (int)(g.hi - g.lo);
-        const int64_t i0 = g.lo + t0;
         double acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -488,21 +392,27 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         // entries) or already summed into y by rest_kernel (remainder-heavy matrices).
         if constexpr (REST == 2) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = t0 + r < rows ? a.y[i0 + r] : 0.0;
+            for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? a.y[g.lo + lr(r)] : 0.0;
         } else if constexpr (REST == 1) {
-            warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
-                                S.scratch + warp * WPASS, acc);
-        } else if constexpr (REST == 3) {
-            const int e_lo = __ldg(a.rest_rp + g.lo), e_hi = __ldg(a.rest_rp + g.hi);
-            if (e_hi > e_lo) staged_rest<R, SCALE>(a, S, sc, g.lo, g.hi, e_lo, e_hi, warp, lane, cs, cphase, acc);
+            if constexpr (IL) {  // the warp's rows are R runs of 32
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int64_t lo = g.lo + (int64_t)CONSUMERS * r;
+                    if (lo >= g.hi) break;
+                    double a1[1] = {0.0};
+                    warp_rest<1, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo,
+                                        min(lo + CONSUMERS, g.hi), warp, lane, S.scratch + warp * WPASS, a1);
+                    acc[r] = a1[0];
+                }
+            } else {
+                warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
+                                    S.scratch + warp * WPASS, acc);
+            }
         }
 
-        // diagonal segments, stored order.  k0: this warp's block's first segment,
-        // nseg its count, J the number of ring stages the tile takes (the largest
-        // count over the tile's blocks; = nseg when the tile is inside one block).
-        // [k0, k1): the ring stages of the tile; [k0, kw): this warp's block's
-        // segments (MB: k1 - k0 is the largest segment count over the tile's
-        // blocks; otherwise kw = k1, the one block's segments).
+        // diagonal segments, stored order.  [k0, k1): the ring stages of the tile;
+        // [k0, kw): this warp's block's segments (MB: k1 - k0 is the largest
+        // segment count over the tile's blocks; otherwise kw = k1, the one block's).
         int k0, k1, kw;
         if constexpr (MB) {  // warp-uniform: bl % (32 R) == 0
             const int64_t bw = (int64_t)g.b + t0 / (int)a.bl;
@@ -515,7 +425,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             k0 = __ldg(a.dia_ptr + g.b);
             k1 = kw = __ldg(a.dia_ptr + g.b + 1);
         }
-        const double* xrow = a.x + i0;
+        const double* xrow = a.x + g.lo;
         const bool full = rows == TILE;  // warp-uniform: no per-row predicates needed
         for (int kb0 = k0; kb0 < k1; kb0 += 32) {
             // the next <= 32 offsets of the block: one coalesced load, then shuffles
@@ -534,12 +444,12 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                     if (u < nv) {
                         if (full && g.lo + o >= xlo_valid && g.hi + o <= xhi_valid) {  // common case
 #pragma unroll
-                            for (int r = 0; r < R; ++r) xv[u][r] = __ldg(xrow + r + o);
+                            for (int r = 0; r < R; ++r) xv[u][r] = __ldg(xrow + lr(r) + o);
                         } else {
 #pragma unroll
                             for (int r = 0; r < R; ++r) {
-                                const int64_t j = i0 + r + o;
-                                if (t0 + r < rows && j >= xlo_valid && j < xhi_valid) xv[u][r] = __ldg(xrow + r + o);
+                                const int64_t j = g.lo + lr(r) + o;
+                                if (lr(r) < rows && j >= xlo_valid && j < xhi_valid) xv[u][r] = __ldg(xrow + lr(r) + o);
                             }
                         }
                     }
@@ -548,36 +458,23 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                 for (int u = 0; u < XG; ++u) {
                     if (u < ng) {
                         mbar_wait(&S.full[cs], cphase);
-                        const double* st = S.ring + cs * STRIDE + t0;
-                        // odd bl: the slice may sit one slot in (see the producer)
-                        // (bl odd: k*bl has k's parity; tile starts are even for R >= 2)
-                        const int sh = !ODD ? 0
-                                            : R >= 2 ? (kb0 + kg + u) & 1 : ((kb0 + kg + u) ^ (int)(g.lo - g.b0)) & 1;
+                        const double* st = S.ring + cs * STRIDE;
                         double v[R];
-                        if (ODD && R >= 2) {
-                            // the slice may start one slot in (sh): this thread's values
-                            // are then e[1..R] of its aligned R-group -- 16-byte loads of
-                            // e[0..R-1] (conflict-free), e[R] from the next lane's e[0]
-                            double e[R];
+                        if constexpr (IL) {
+                            // odd bl: the slice may sit one slot in (see the producer;
+                            // k*bl has k's parity, tile starts are even for R >= 2)
+                            const int sh = !ODD ? 0
+                                                : R >= 2 ? (kb0 + kg + u) & 1
+                                                         : ((kb0 + kg + u) ^ (int)(g.lo - g.b0)) & 1;
+#pragma unroll
+                            for (int r = 0; r < R; ++r) v[r] = st[lr(r) + sh];
+                        } else {
 #pragma unroll
                             for (int h = 0; h < R / 2; ++h) {
-                                const double2 t = reinterpret_cast<const double2*>(st)[h];
-                                e[2 * h] = t.x;
-                                e[2 * h + 1] = t.y;
-                            }
-                            double last = __shfl_down_sync(0xffffffffu, e[0], 1);
-                            if (lane == 31 && sh) last = st[R];
-#pragma unroll
-                            for (int r = 0; r < R; ++r) v[r] = sh ? (r + 1 < R ? e[r + 1] : last) : e[r];
-                        } else if (R >= 2) {
-#pragma unroll
-                            for (int h = 0; h < R / 2; ++h) {
-                                const double2 t = reinterpret_cast<const double2*>(st)[h];
+                                const double2 t = reinterpret_cast<const double2*>(st + t0)[h];
                                 v[2 * h] = t.x;
                                 v[2 * h + 1] = t.y;
                             }
-                        } else {
-                            v[0] = st[sh];
                         }
                         if (u < nv) {
 #pragma unroll
@@ -603,31 +500,35 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             }
         }
 
-        if (t0 < rows) {
-            if (R >= 2 && (ODD ? ((uintptr_t)(a.y + i0) & 15) == 0 : a.y_vec_ok) && t0 + R - 1 < rows) {
+        if constexpr (IL) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (lr(r) < rows) __stcs(a.y + g.lo + lr(r), acc[r]);
+        } else if (t0 < rows) {
+            if (a.y_vec_ok && t0 + R - 1 < rows) {
 #pragma unroll
                 for (int h = 0; h < R / 2; ++h)
-                    __stcs(reinterpret_cast<double2*>(a.y + i0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));
+                    __stcs(reinterpret_cast<double2*>(a.y + g.lo + t0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));
             } else {
 #pragma unroll
                 for (int r = 0; r < R; ++r)
-                    if (t0 + r < rows) __stcs(a.y + i0 + r, acc[r]);
+                    if (t0 + r < rows) __stcs(a.y + g.lo + t0 + r, acc[r]);
             }
-            if (a.peer_lo || a.peer_hi) {  // halo rows also to the neighbours (peer memory)
+        }
+        if (a.peer_lo || a.peer_hi) {  // halo rows also to the neighbours (peer memory)
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int64_t i = i0 + r;
-                    if (t0 + r >= rows) continue;
-                    if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc[r];
-                    if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc[r];
-                }
+            for (int r = 0; r < R; ++r) {
+                const int64_t i = g.lo + lr(r);
+                if (lr(r) >= rows) continue;
+                if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc[r];
+                if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc[r];
             }
         }
         if (NORM) {
             double s = 0.0;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                if (t0 + r < rows) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
+                if (lr(r) < rows) s = __dadd_rn(s, __dmul_rn(acc[r], acc[r]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
             // the tile's 8 warp partials in warp order, one consumer barrier per tile
@@ -676,7 +577,6 @@ void launch_rr(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, c
 template <int R, int LAY>
 void launch_m(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if (a.init_y) launch_rr<R, 2, LAY>(a, grid, smem, scale, norm, st);
-    else if (a.has_rest && a.rest_staged) launch_rr<R, 3, LAY>(a, grid, smem, scale, norm, st);
     else if (a.has_rest) launch_rr<R, 1, LAY>(a, grid, smem, scale, norm, st);
     else launch_rr<R, 0, LAY>(a, grid, smem, scale, norm, st);
 }
@@ -735,7 +635,6 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.init_y = 0;
-    a.rest_staged = 0;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;  // (odd bl: tiles may start on odd rows, tested per thread)
     a.peer_lo = peer.lo;
     a.peer_hi = peer.hi;
@@ -750,11 +649,11 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     // Remainder mode (hdcg_set_kernel_policy / HDCG_REST_MODE override the default):
     // 2 summed first by rest_kernel -- the default for remainder-heavy matrices (>= 1
     // entry per 4 rows); 1 loaded from global memory by the consumers -- the default
-    // otherwise; 3 staged through the ring by the producer.
+    // otherwise.  (A third mode, the producer staging the remainder through the
+    // ring, measured 33% at config 3 and was removed: profiles/README.md.)
     static const int env_mode = getenv("HDCG_REST_MODE") ? atoi(getenv("HDCG_REST_MODE")) : 0;
     const int req = g_rest_mode ? g_rest_mode : env_mode;
-    const int mode = req >= 1 && req <= 3 ? req : (m.nnz_rest * 4 >= m.n_rows ? 2 : 1);
-    a.rest_staged = a.has_rest && mode == 3;
+    const int mode = req >= 1 && req <= 2 ? req : (m.nnz_rest * 4 >= m.n_rows ? 2 : 1);
     const bool split = a.has_rest && mode == 2;
     auto rest_rows = [&](int64_t tb, int64_t te, cudaStream_t s) {
         // rows covered by the tile range (tiles are contiguous in rows)

@@ -52,7 +52,7 @@ EXPORTS = (
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
-REST_DEFAULT, REST_GLOBAL, REST_SPLIT, REST_STAGED = 0, 1, 2, 3
+REST_DEFAULT, REST_GLOBAL, REST_SPLIT = 0, 1, 2
 
 
 class LibraryMissing(ImportError):
@@ -603,5 +603,5 @@ def membench(n: int, mode: str = "direct", n_loops: int = 20, n_ites: int = 1000
 def set_kernel_policy(policy: int, rest_mode: int = 0):
     """policy: 0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA kernel only.
     rest_mode (TMA kernel's CSR remainder): 0 default, 1 global loads, 2 summed first
-    by a separate kernel, 3 staged through the TMA ring."""
+    by a separate kernel."""
     check(lib().hdcg_set_kernel_policy(policy + 16 * rest_mode))

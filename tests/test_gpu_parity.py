@@ -334,7 +334,7 @@ def test_config3_quasi_diagonal(port):
         assert y.tobytes() == want.tobytes()
         assert_within_tol(y, yc, rp, col, val, x)
         try:  # every remainder mode at scale
-            for mode in (H.REST_GLOBAL, H.REST_SPLIT, H.REST_STAGED):
+            for mode in (H.REST_GLOBAL, H.REST_SPLIT):
                 H.set_kernel_policy(H.POLICY_TMA, mode)
                 for _ in range(3):
                     assert H.spmv_mhdc(m, x).tobytes() == want.tobytes(), (bl, mode)
@@ -565,11 +565,10 @@ def test_reference_acceptance_through_gpu_shim():
     assert "all 8 criteria passed" in r.stdout
 
 
-@pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT, H.REST_STAGED])
+@pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT])
 def test_remainder_paths(port, rest_mode):
     """The TMA kernel's ways of summing the CSR remainder (consumers load it from
-    global memory; a separate rest_kernel sums it into y first; the producer stages it
-    through the TMA ring)
+    global memory; a separate rest_kernel sums it into y first)
     must all be bitwise equal to the oracle, sparse and heavy."""
     H.set_kernel_policy(H.POLICY_TMA, rest_mode)
     try:
