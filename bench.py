@@ -350,7 +350,7 @@ def run_ours(a):
     # ---- e2e through the public host API: H2D x, SpMV, D2H y per step ----------------
     e2e_steps = max(1, min(a.steps, 5))
     x_host = torch.empty(g1 - g0, dtype=torch.float64).pin_memory()
-    x_host.copy_(xbuf[g0 - (row0 - halo):g1 - (row0 - halo)].cpu())
+    x_host.copy_(it.bufs[0][g0 - (row0 - halo):g1 - (row0 - halo)].cpu())
     y_host = torch.empty(rows, dtype=torch.float64).pin_memory()
     if world == 1:
         def e2e_call():
