@@ -72,6 +72,7 @@ typedef struct {
     int64_t tile_rows;  /* rows per tile (tiles never straddle a block) */
     int64_t blocks_per_tile; /* >1 when bl < tile_rows */
     int64_t device_bytes;
+    int64_t max_seg_per_block; /* most segments in one block (selects the SpMV kernel) */
 } hdcg_info;
 
 /* ---- runtime ------------------------------------------------------------ */

@@ -486,6 +486,7 @@ hdcg_status hdcg_get_info(hdcg_matrix h, hdcg_info* info) {
         info->tile_rows = t.tile_rows;
         info->blocks_per_tile = t.blocks_per_tile > 0 ? t.blocks_per_tile : 1;
         info->device_bytes = m->device_bytes;
+        info->max_seg_per_block = m->max_seg_per_block;
     });
 }
 

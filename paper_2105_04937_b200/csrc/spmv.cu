@@ -230,18 +230,16 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 //                         1024/bl whole blocks per tile)
 //   other bl >= 512      : 2 rows/thread, 512-row tiles
 //   bl in [256,512)      : 1 row/thread, 256-row tiles, 2 tiles per block
-//   even bl < 256        : 2 rows/thread, 512/bl whole blocks per tile
-//   odd bl < 256         : 1 row/thread, 256/bl whole blocks per tile
+//   other bl < 256       : 1 row/thread, 256/bl whole blocks per tile
 // (odd bl: a slice of segment k starts on an odd slot when k is odd, so both
 // kernels fall back to 8-byte segment loads / y stores there)
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
-    const bool even = m.bl % 2 == 0;
     const int64_t t4 = 4 * SPMV_THREADS;
     if (m.max_seg_per_block <= 8 && (m.bl >= t4 || (m.bl >= 128 && m.bl % 4 == 0 && t4 % m.bl == 0)))
         t.rows_per_thread = 4;
-    else if (m.bl >= 2 * SPMV_THREADS || (even && m.bl < SPMV_THREADS)) t.rows_per_thread = 2;
-    else t.rows_per_thread = 1;
+    else if (m.bl >= 2 * SPMV_THREADS) t.rows_per_thread = 2;
+    else t.rows_per_thread = 1;  // incl. bl < 256: 256/bl whole blocks per tile (spmv_blk_kernel)
     t.tile_rows = (int64_t)SPMV_THREADS * t.rows_per_thread;
     if (m.bl >= t.tile_rows) {
         t.tiles_per_block = ceil_div(m.bl, t.tile_rows);

@@ -257,6 +257,87 @@ __global__ void __launch_bounds__(CONSUMERS, MINB) rest_kernel(const TmaArgs a, 
         if (i0 + r < hi) a.y[i0 + r] = acc[r];
 }
 
+// Software-pipelined remainder sums (the default for remainder-heavy matrices and
+// CSR).  rest_kernel pays three dependent round trips per 32 rows (row pointers ->
+// columns/values -> x gathers); here a warp owns G runs of 32 rows (one contiguous
+// entry range), stages their row pointers in shared memory once, and walks the range
+// in passes of 32*PER entries with the next pass's columns loaded while this pass's
+// gathers and values are in flight -- one round trip per pass.  Lanes own the rows
+// of the current 32-row run; a pass's products go to the warp's scratch and each
+// lane adds those of its row in stored order (runs finished inside the pass are
+// stored and the lanes move to the next run).  Same operations in the same order as
+// warp_rest: bitwise equal.
+template <bool SCALE, int MINB, int G, int PER>
+__global__ void __launch_bounds__(CONSUMERS, MINB) rest_pipe_kernel(const TmaArgs a, int64_t row_lo, int64_t row_hi) {
+    constexpr int PASS = 32 * PER;
+    constexpr int WROWS = 32 * G;
+    __shared__ double scratch_all[CONSUMER_WARPS][PASS];
+    __shared__ int32_t rp_all[CONSUMER_WARPS][WROWS + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* scratch = scratch_all[warp];
+    int32_t* rps = rp_all[warp];
+    const int64_t w0 = row_lo + ((int64_t)blockIdx.x * CONSUMER_WARPS + warp) * WROWS;
+    if (w0 >= row_hi) return;
+    const int nrows = (int)min((int64_t)WROWS, row_hi - w0);
+    for (int i = lane; i <= WROWS; i += 32) rps[i] = __ldg(a.rest_rp + w0 + min(i, nrows));
+    __syncwarp();
+    const double sc = SCALE ? *a.x_scale : 1.0;
+    const int e0 = rps[0], e1 = rps[WROWS];
+    int g = 0;  // current 32-row run
+    int kb = rps[lane], ke = rps[lane + 1];
+    int gend = rps[32];  // first entry past the run (warp-uniform)
+    double acc = 0.0;
+    int32_t cn[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int q = e0 + lane + 32 * j;
+        cn[j] = q < e1 ? __ldcs(a.rest_col + q) : 0;
+    }
+    int c = e0;
+    do {
+        int32_t cl[PER];
+        double xl[PER], vl[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) cl[j] = cn[j];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int q = c + lane + 32 * j;
+            xl[j] = q < e1 ? __ldg(a.x + ((int64_t)cl[j] - a.row0)) : 0.0;
+            vl[j] = q < e1 ? __ldcs(a.rest_val + q) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {  // the next pass's columns
+            const int q = c + PASS + lane + 32 * j;
+            cn[j] = q < e1 ? __ldcs(a.rest_col + q) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            double xv = xl[j];
+            if (SCALE) xv = __dmul_rn(xv, sc);
+            scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
+        }
+        __syncwarp();
+        const int cend = c + PASS;
+        while (true) {
+            const int p0 = max(kb, c), p1 = min(ke, cend);
+            for (int p = p0; p < p1; ++p) acc = __dadd_rn(acc, scratch[p - c]);
+            if (gend > cend || g >= G) break;  // the run continues in the next pass
+            const int r = 32 * g + lane;
+            if (r < nrows) a.y[w0 + r] = acc;
+            acc = 0.0;
+            if (++g >= G || 32 * g >= nrows) {
+                g = G;
+                break;
+            }
+            kb = rps[32 * g + lane];
+            ke = rps[32 * g + lane + 1];
+            gend = rps[min(32 * g + 32, WROWS)];
+        }
+        __syncwarp();
+        c = cend;
+    } while (c < e1);
+}
+
 // REST: 0 no remainder, 1 remainder summed here from global memory (fused),
 // 2 remainder sums already in y (rest_kernel ran first)
 // LAY: tile layout.  0 tiles inside one block, even bl; 1 multi-block tiles
@@ -552,6 +633,264 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     if (a.peer_lo || a.peer_hi) __threadfence_system();
 }
 
+// ---------------------------------------------------------------------------
+// Small blocks (8 <= bl < 256 outside the multi-block layout -- the paper's
+// recommended bl = 50 / 100, and hdcmv's default bl = 100,
+// hdcmv.cpp:148): a tile is G = 256/bl whole blocks, and its segments are ONE
+// contiguous run of the segment array, seg[dia_ptr[b0]*bl, dia_ptr[b0+G]*bl).
+// A ring stage holds a whole tile: the producer warp stages the tile's block
+// starts (relative) and offsets in the stage header with plain loads/stores, and
+// one cp.async.bulk brings the values (16-byte aligned: an odd start is copied
+// from one slot earlier, the shift is in the header).  Consumer thread t owns
+// tile row t (block q = t / bl, slot t % bl -- fixed for the whole kernel) and
+// reads everything but x from shared memory: no dependent global loads before
+// its x gathers.  Same per-row operations in the same order as spmv_kernel.
+constexpr int BLK_MAX_SEG = 16;  // eligibility: max segments per block (27 segments measured slower)
+constexpr int BLK_MAX_G = 32;    // bl >= 8
+constexpr int BLK_XG = 8;        // x gathers in flight per thread
+
+__host__ __device__ inline int blk_vals_stride(int max_seg, int G, int bl) {  // doubles, even
+    return ((max_seg * G * bl + 2) + 1) & ~1;
+}
+__host__ __device__ inline int blk_hdr_ints(int max_seg, int G) {  // 4-int aligned
+    return ((4 + G + 1 + max_seg * G) + 3) & ~3;
+}
+
+template <bool SCALE, bool NORM, int REST>
+__global__ void __launch_bounds__(THREADS, 3) spmv_blk_kernel(const TmaArgs a, int max_seg) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int NS = a.nstage;
+    const int G = a.blocks_per_tile;
+    const int bl = (int)a.bl;
+    const int VST = blk_vals_stride(max_seg, G, bl);
+    const int HST = blk_hdr_ints(max_seg, G);
+    const size_t stage_bytes = sizeof(double) * VST + sizeof(int32_t) * HST;  // multiple of 16
+    double* scratch = reinterpret_cast<double*>(smem_raw + stage_bytes * NS);  // CONSUMER_WARPS * WPASS
+    double* wsum = scratch + (a.has_rest ? CONSUMER_WARPS * WPASS : 0);          // 2 * CONSUMER_WARPS
+    uint64_t* full = reinterpret_cast<uint64_t*>(wsum + 2 * CONSUMER_WARPS);
+    uint64_t* empty = full + NS;
+    auto vals = [&](int s) { return reinterpret_cast<double*>(smem_raw + stage_bytes * s); };
+    // header: [0] value shift, [1] segment count, [2] / [3] least / greatest offset,
+    // [4 .. 4+G] block starts (relative), then the offsets
+    auto hdr = [&](int s) { return reinterpret_cast<int32_t*>(smem_raw + stage_bytes * s + sizeof(double) * VST); };
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMER_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == CONSUMER_WARPS) {
+        // ------------------------------ producer warp ------------------------------
+        const uint64_t policy = evict_first_policy();
+        constexpr int OFR = 4;  // offsets per lane held in registers (nk <= 128; more: a loop)
+        int ps = 0;
+        uint32_t pphase = 0;
+        bool p_wrapped = false;
+        // the next tile's block starts are loaded while this tile's offsets are, and
+        // both before the wait for a free stage (a deeper look-ahead measured no faster)
+        int tile = a.tile_begin + blockIdx.x;
+        auto starts = [&](int tl, int& dp, int& k1) {
+            if (tl >= a.tile_end) return;
+            const int64_t b0 = (int64_t)tl * G;
+            const int nb = (int)min((int64_t)G, a.n_blocks - b0);
+            dp = lane < nb ? __ldg(a.dia_ptr + b0 + lane) : 0;
+            k1 = __ldg(a.dia_ptr + b0 + nb);
+        };
+        int dp_n = 0, k1_n = 0;
+        starts(tile, dp_n, k1_n);
+        for (; tile < a.tile_end; tile += gridDim.x) {
+            const int64_t b0 = (int64_t)tile * G;
+            const int nb = (int)min((int64_t)G, a.n_blocks - b0);
+            const int dp = dp_n, k1 = k1_n;
+            const int k0 = __shfl_sync(0xffffffffu, dp, 0);
+            const int nk = k1 - k0;
+            int ofr[OFR];
+#pragma unroll
+            for (int u = 0; u < OFR; ++u) {
+                const int j = lane + 32 * u;
+                ofr[u] = j < nk ? __ldg(a.dia_off + k0 + j) : 0;
+            }
+            starts(tile + gridDim.x, dp_n, k1_n);
+            if (p_wrapped) mbar_wait(&empty[ps], pphase ^ 1u);
+            int32_t* h = hdr(ps);
+            const int sh = (int)(((int64_t)k0 * bl) & 1);
+            if (lane < nb) h[4 + lane] = dp - k0;
+            int32_t* ho = h + 4 + G + 1;
+            int omin = 0x7fffffff, omax = -0x7fffffff;
+#pragma unroll
+            for (int u = 0; u < OFR; ++u) {
+                const int j = lane + 32 * u;
+                if (j < nk) {
+                    ho[j] = ofr[u];
+                    omin = min(omin, ofr[u]);
+                    omax = max(omax, ofr[u]);
+                }
+            }
+            for (int j = lane + 32 * OFR; j < nk; j += 32) {
+                const int o = __ldg(a.dia_off + k0 + j);
+                ho[j] = o;
+                omin = min(omin, o);
+                omax = max(omax, o);
+            }
+            omin = __reduce_min_sync(0xffffffffu, omin);
+            omax = __reduce_max_sync(0xffffffffu, omax);
+            if (lane == 0) {
+                h[0] = sh;
+                h[1] = nk;
+                h[2] = omin;
+                h[3] = omax;
+                h[4 + nb] = nk;
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (nk > 0) {
+                    const uint32_t bytes = (uint32_t)((((int64_t)nk * bl + sh + 1) & ~int64_t(1)) * 8);
+                    mbar_expect_tx(&full[ps], bytes);
+                    bulk_g2s(vals(ps), a.seg + (int64_t)k0 * bl - sh, bytes, &full[ps], policy);
+                } else {
+                    mbar_arrive(&full[ps]);
+                }
+            }
+            if (++ps == NS) {
+                ps = 0;
+                pphase ^= 1u;
+                p_wrapped = true;
+            }
+        }
+        return;
+    }
+
+    // -------------------------------- consumers --------------------------------
+    const int t = threadIdx.x;
+    const int q = t / bl, l = t - q * bl;  // this thread's block in the tile and slot in it
+    double sc = 1.0;
+    if (SCALE) sc = *a.x_scale;
+    const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;
+    int cs = 0;
+    uint32_t cphase = 0, par = 0;
+    // REST == 1: the remainder entry range of this warp's rows, loaded one tile ahead
+    // (most tiles of a light remainder have none: no dependent load on their path)
+    auto probe = [&](int tl, int& e0, int& e1) {
+        e0 = e1 = 0;
+        if (REST != 1 || tl >= a.tile_end) return;
+        const int64_t lo_t = (int64_t)tl * G * bl;
+        const int64_t hi_t = min(lo_t + (int64_t)G * bl, a.n_rows);
+        const int64_t w_lo = min(lo_t + 32 * warp, hi_t), w_hi = min(w_lo + 32, hi_t);
+        e0 = __ldg(a.rest_rp + w_lo);
+        e1 = __ldg(a.rest_rp + w_hi);
+    };
+    int pe0, pe1;
+    probe(a.tile_begin + blockIdx.x, pe0, pe1);
+    for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
+        const int64_t b0 = (int64_t)tile * G;
+        const int nb = (int)min((int64_t)G, a.n_blocks - b0);
+        const int64_t lo = b0 * bl;
+        const int64_t hi = min(lo + (int64_t)nb * bl, a.n_rows);
+        const int64_t i = lo + t;
+        const bool active = q < nb && i < hi;
+        double acc = 0.0;
+        if constexpr (REST == 2) {
+            if (active) acc = a.y[i];
+        } else if constexpr (REST == 1) {
+            const bool any = pe0 < pe1;
+            probe(tile + gridDim.x, pe0, pe1);
+            if (any) {
+                double a1[1] = {0.0};
+                warp_rest<1, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo, hi, warp, lane,
+                                    scratch + warp * WPASS, a1);
+                acc = a1[0];
+            }
+        }
+        mbar_wait(&full[cs], cphase);
+        const int32_t* h = hdr(cs);
+        const int kst = active ? h[4 + q] : 0, kend = active ? h[4 + q + 1] : 0;
+        const int cnt = kend - kst;
+        const int cmax = __reduce_max_sync(0xffffffffu, cnt);
+        const int32_t* op = h + 4 + G + 1 + kst;             // this row's offsets
+        const double* vp = vals(cs) + h[0] + l + kst * bl;  // this row's first value
+        // tile-uniform: every x index of the tile in range (the common case)
+        const bool inr = lo + h[2] >= xlo_valid && hi + h[3] <= xhi_valid;
+        const double* xr = a.x + i;
+        for (int j0 = 0; j0 < cmax; j0 += BLK_XG) {
+            double xv[BLK_XG];
+#pragma unroll
+            for (int u = 0; u < BLK_XG; ++u) {
+                xv[u] = 0.0;
+                if (j0 + u < cnt) {
+                    const int o = op[j0 + u];
+                    if (inr || (i + o >= xlo_valid && i + o < xhi_valid)) xv[u] = __ldg(xr + o);
+                }
+            }
+            const double* vq = vp + j0 * bl;
+#pragma unroll
+            for (int u = 0; u < BLK_XG; ++u) {
+                if (j0 + u < cnt) {
+                    double xx = xv[u];
+                    if (SCALE) xx = __dmul_rn(xx, sc);
+                    acc = __dadd_rn(acc, __dmul_rn(*vq, xx));
+                }
+                vq += bl;
+            }
+        }
+        asm volatile("" ::"d"(acc));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cs]);
+        if (++cs == NS) {
+            cs = 0;
+            cphase ^= 1u;
+        }
+        if (active) {
+            __stcs(a.y + i, acc);
+            if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc;
+            if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc;
+        }
+        if (NORM) {  // spmv_kernel's order: warp shuffle tree, then the warps in order
+            double s = active ? __dmul_rn(acc, acc) : 0.0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, off));
+            double* ws = wsum + par * CONSUMER_WARPS;
+            if (lane == 0) ws[warp] = s;
+            consumer_sync();
+            if (threadIdx.x == 0) {
+                double tot = 0.0;
+#pragma unroll
+                for (int w = 0; w < CONSUMER_WARPS; ++w) tot = __dadd_rn(tot, ws[w]);
+                a.tile_sumsq[tile] = tot;
+            }
+            par ^= 1;
+        }
+    }
+    if (a.peer_lo || a.peer_hi) __threadfence_system();
+}
+
+template <bool SCALE, bool NORM, int REST>
+void launch_blk(const TmaArgs& a, int max_seg, int grid, size_t smem, cudaStream_t st) {
+    auto k = spmv_blk_kernel<SCALE, NORM, REST>;
+    static bool configured = false;
+    if (!configured) {
+        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        configured = true;
+    }
+    k<<<grid, THREADS, smem, st>>>(a, max_seg);
+}
+
+template <int REST>
+void launch_blk_r(const TmaArgs& a, int max_seg, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
+    if (scale) {
+        if (norm) launch_blk<true, true, REST>(a, max_seg, grid, smem, st);
+        else launch_blk<true, false, REST>(a, max_seg, grid, smem, st);
+    } else {
+        if (norm) launch_blk<false, true, REST>(a, max_seg, grid, smem, st);
+        else launch_blk<false, false, REST>(a, max_seg, grid, smem, st);
+    }
+}
+
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM, REST, LAY>;
@@ -611,7 +950,11 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     const int R = t.rows_per_thread;
     if (t.tile_rows != (int64_t)CONSUMERS * R) return false;
     // multi-block tiles: R = 4 (bl in {128, 256, 512}, tiling_of) only
-    if (t.tiles_per_block <= 0 && (R != 4 || t.blocks_per_tile <= 0 || m.bl % (32 * R) != 0)) return false;
+    // small blocks, 8 <= bl < 256: whole-tile stages (spmv_blk_kernel); HDCG_BLK=0 disables (A/B)
+    const char* eb = getenv("HDCG_BLK");
+    const bool blk = (!eb || atoi(eb) != 0) && t.blocks_per_tile > 0 && R == 1 && m.bl >= CONSUMERS / BLK_MAX_G &&
+                     m.bl < CONSUMERS && m.max_seg_per_block <= BLK_MAX_SEG;
+    if (!blk && t.tiles_per_block <= 0 && (R != 4 || t.blocks_per_tile <= 0 || m.bl % (32 * R) != 0)) return false;
     if (tile_end <= tile_begin) return true;
     TmaArgs a;
     a.dia_ptr = m.dia_ptr;
@@ -661,14 +1004,37 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         tile_rows(tb, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m.bl, m.n_rows, &r0, &dummy);
         tile_rows(te - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m.bl, m.n_rows, &dummy, &r1);
         r0 = std::min(r0, m.n_rows);
-        if (r1 > r0) {
-            // 5 CTAs/SM (48 registers), one row per lane, 8 gathers per lane in flight:
-            // the best of the variants measured (profiles/README.md, v8)
-            const unsigned nb = (unsigned)ceil_div(r1 - r0, CONSUMERS);
-            if (x_scale) rest_kernel<true, 5, 1, 8><<<nb, CONSUMERS, 0, s>>>(a, r0, r1);
-            else rest_kernel<false, 5, 1, 8><<<nb, CONSUMERS, 0, s>>>(a, r0, r1);
-            HDCG_LAUNCH_CHECK("rest_kernel");
+        if (r1 <= r0) return;
+        // HDCG_REST_VARIANT: A/B knob, read per call (tests switch it in-process)
+        const char* ev = getenv("HDCG_REST_VARIANT");
+        const int variant = ev ? atoi(ev) : 1;
+        auto pipe = [&](auto kern, int g) {
+            kern<<<(unsigned)ceil_div(r1 - r0, (int64_t)CONSUMERS * g), CONSUMERS, 0, s>>>(a, r0, r1);
+        };
+        switch (variant) {
+            case 0: {  // rest_kernel: 5 CTAs/SM, one row per lane, 8 gathers per lane in flight
+                const unsigned nb = (unsigned)ceil_div(r1 - r0, CONSUMERS);
+                if (x_scale) rest_kernel<true, 5, 1, 8><<<nb, CONSUMERS, 0, s>>>(a, r0, r1);
+                else rest_kernel<false, 5, 1, 8><<<nb, CONSUMERS, 0, s>>>(a, r0, r1);
+                break;
+            }
+            case 2:
+                if (x_scale) pipe(rest_pipe_kernel<true, 3, 4, 8>, 4);
+                else pipe(rest_pipe_kernel<false, 3, 4, 8>, 4);
+                break;
+            case 3:
+                if (x_scale) pipe(rest_pipe_kernel<true, 4, 8, 4>, 8);
+                else pipe(rest_pipe_kernel<false, 4, 8, 4>, 8);
+                break;
+            case 4:
+                if (x_scale) pipe(rest_pipe_kernel<true, 3, 16, 8>, 16);
+                else pipe(rest_pipe_kernel<false, 3, 16, 8>, 16);
+                break;
+            default:
+                if (x_scale) pipe(rest_pipe_kernel<true, 3, 8, 8>, 8);
+                else pipe(rest_pipe_kernel<false, 3, 8, 8>, 8);
         }
+        HDCG_LAUNCH_CHECK("rest_kernel");
     };
     // ring of segment slices: ~64 KB per CTA, 3 CTAs per SM (tunable for profiling)
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
@@ -677,6 +1043,31 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         TmaArgs b = base;
         b.tile_begin = (int)tb;
         b.tile_end = (int)te;
+        if (blk) {
+            const int G = (int)t.blocks_per_tile, ms = (int)std::max<int64_t>(1, m.max_seg_per_block);
+            const size_t stage = sizeof(double) * blk_vals_stride(ms, G, (int)m.bl) + sizeof(int32_t) * blk_hdr_ints(ms, G);
+            const size_t fixed = sizeof(double) * ((b.has_rest ? CONSUMER_WARPS * WPASS : 0) + 2 * CONSUMER_WARPS) +
+                                 sizeof(uint64_t) * 2 * 32;
+            // >= 3 stages per CTA: fewer CTAs per SM when the stages are large
+            int want = want_ctas;
+            auto stages_for = [&](int w) {
+                const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / w - 1024;
+                return std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
+            };
+            while (want > 1 && stages_for(want) < 3) --want;
+            b.nstage = stages_for(want);
+            const size_t smem = stage * b.nstage + fixed;
+            const int fit = (int)((227 * 1024) / (smem + 1024));
+            const int per_sm = std::max(1, std::min(want, fit));
+            const int64_t cap = (int64_t)sm_count() * per_sm;
+            const int grid = (int)(te - tb < cap ? te - tb : cap);
+            const bool sc = x_scale != nullptr, nm = tile_sumsq != nullptr;
+            if (b.init_y) launch_blk_r<2>(b, ms, grid, smem, sc, nm, s);
+            else if (b.has_rest) launch_blk_r<1>(b, ms, grid, smem, sc, nm, s);
+            else launch_blk_r<0>(b, ms, grid, smem, sc, nm, s);
+            HDCG_LAUNCH_CHECK("spmv_blk_kernel");
+            return;
+        }
         const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
         const size_t fixed = smem_bytes(R, 0, b.has_rest);
         const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
@@ -693,6 +1084,9 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     };
     if (split) {
         rest_rows(tile_begin, tile_end, st);
+        // no segments (a CSR, spmv_csr): rest_kernel's sums are y -- unless the
+        // TMA kernel's epilogue is needed (fused norm, peer halo stores)
+        if (m.n_seg == 0 && !tile_sumsq && !peer.lo && !peer.hi) return true;
         a.has_rest = 0;
         a.init_y = 1;
     }

@@ -81,7 +81,7 @@ class Info(C.Structure):
                 ("n_blocks", C.c_int64), ("n_seg", C.c_int64), ("nnz_rest", C.c_int64),
                 ("dia_slots", C.c_int64), ("nnz_input", C.c_int64), ("n_tiles", C.c_int64),
                 ("tile_rows", C.c_int64), ("blocks_per_tile", C.c_int64),
-                ("device_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("max_seg_per_block", C.c_int64)]
 
 
 _lib = None
@@ -532,10 +532,15 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     b = lambda v: str(v).lower()  # noqa: E731
     inside = info.bl >= info.tile_rows  # tiles inside one block, else whole blocks per tile
     mb = not inside and r == 4 and info.bl % 128 == 0
-    if not ((info.bl >= 256 and inside) or mb):
+    blk = not inside and r == 1 and 8 <= info.bl < 256 and info.max_seg_per_block <= 16
+    if not ((info.bl >= 256 and inside) or mb or blk):
         return [f"hdcg::spmv_kernel<{r},{b(scale)},{b(norm)}>"]
     rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
-    ks = ["hdcg::rest_kernel"] if rest == 2 else []
+    ks = ["hdcg::rest_pipe_kernel"] if rest == 2 else []
+    if rest == 2 and info.n_seg == 0 and not norm:
+        return ks  # a CSR: the remainder kernel's sums are y
+    if blk:
+        return ks + [f"hdcg::spmv_blk_kernel<{b(scale)},{b(norm)},{rest}>"]
     lay = 1 if mb else (2 if info.bl % 2 else 0)  # tile layout: inside one block / multi-block / odd bl
     ks.append(f"hdcg::spmv_tma_kernel<{r},{b(scale)},{b(norm)},{rest},{lay}>")
     return ks

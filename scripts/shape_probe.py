@@ -18,8 +18,9 @@ st = torch.cuda.current_stream().cuda_stream
 flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 cases = [("lap255_hdc", 255, None), ("lap256_bl4095", 256, 4095), ("lap256_bl2047", 256, 2047),
          ("lap256_bl192", 256, 192), ("lap256_bl4096", 256, 4096)]
-if len(sys.argv) > 1:
-    cases = [c for c in cases if c[0] in sys.argv[1:]]
+if len(sys.argv) > 1:  # named cases, or any "lap256_bl<N>"
+    named = {c[0]: c for c in cases}
+    cases = [named.get(a) or (a, 256, int(a.split("_bl")[1])) for a in sys.argv[1:]]
 for label, g, bl in cases:
     rp, col, val = synth.laplacian7(g, g, g)
     n = len(rp) - 1

@@ -489,7 +489,8 @@ def test_power_iteration_matches_oracle(port):
 
 
 # ---------------------------------------------------------------------------
-# the two SpMV kernels (general spmv_kernel, TMA-fed spmv_tma_kernel) agree bitwise
+# the SpMV kernels (general spmv_kernel, TMA-fed spmv_tma_kernel / spmv_blk_kernel)
+# agree bitwise, y and the per-tile sums of squares
 
 @pytest.mark.parametrize("shape", ["lap", "quasi", "random"])
 def test_kernel_paths_bitwise_identical(port, shape):
@@ -505,7 +506,7 @@ def test_kernel_paths_bitwise_identical(port, shape):
     x = synth.x_vector(n, 7)
     xd = torch.from_numpy(x).cuda()
     try:
-        for bl in (128, 256, 257, 300, 512, 1000, 1001, 1024, 4096, 4097, 2 * n):
+        for bl in (8, 10, 33, 50, 100, 127, 128, 200, 255, 256, 257, 300, 512, 1000, 1001, 1024, 4096, 4097, 2 * n):
             m = H.to_mhdc(A, 0.6, bl)
             ref = port.spmv_mhdc(port.to_mhdc(rp, col, val, 0.6, bl), x)
             outs = []
@@ -521,7 +522,8 @@ def test_kernel_paths_bitwise_identical(port, shape):
                 assert y2.tobytes() == ref.tobytes(), (shape, bl, pol)
             assert outs[0][0].tobytes() == outs[1][0].tobytes(), (shape, bl)
             assert outs[0][1].tobytes() == outs[1][1].tobytes(), (shape, bl)
-            if "tma" in H.spmv_kernels(m.info)[-1]:  # odd bl >= 256 and bl = 128 included
+            last = H.spmv_kernels(m.info)[-1]
+            if "tma" in last or "blk" in last:  # odd bl >= 256, bl = 128, 8 <= bl < 256 included
                 H.set_kernel_policy(H.POLICY_TMA)
                 assert H.spmv_mhdc(m, x).tobytes() == ref.tobytes()
             m.free()
@@ -594,7 +596,7 @@ def _remainder_cases(port):
         vals = np.concatenate([val, rng.uniform(-1, 1, extra)])
         rp2, col2, val2 = synth.coo_to_csr(n, rows, cols, vals)
         x = synth.x_vector(n, 3)
-        for bl in (1024, 4096, 512, 384, 1023):
+        for bl in (1024, 4096, 512, 384, 1023, 100, 9):
             ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
             m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
             assert_mhdc_equal(m, ref, (extra, bl))
@@ -818,3 +820,45 @@ def test_peer_halo_power_iteration_two_processes(tmp_path):
     for r in range(2):
         assert np.load(tmp_path / f"red2_{r}.npy").tobytes() == np.load(tmp_path / "red1_0.npy").tobytes()
         assert bool(np.load(tmp_path / f"ok2_{r}.npy")[0])
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
+def test_remainder_kernel_variants_and_csr(port, variant, monkeypatch):
+    """Every remainder-sum kernel variant (HDCG_REST_VARIANT: 0 rest_kernel, 1-4
+    the software-pipelined rest_pipe_kernel with several run/pass sizes) is bitwise
+    equal to the oracle: M-HDC with a heavy remainder, and pure CSR (no segments:
+    the remainder kernel's sums are y) with skewed row lengths -- empty rows, rows
+    longer than a pass, partial warp ranges -- plain and in power-iteration form."""
+    monkeypatch.setenv("HDCG_REST_VARIANT", variant)
+    H.set_kernel_policy(H.POLICY_TMA, H.REST_SPLIT)
+    try:
+        _remainder_cases(port)
+        H.set_kernel_policy(H.POLICY_AUTO, H.REST_SPLIT)  # tiny CSRs take the general kernel
+        rng = np.random.default_rng(int(variant) + 5)
+        for n in (1, 31, 33, 1000, 4099, 70001):
+            lens = rng.integers(0, 12, n)
+            lens[rng.random(n) < 0.2] = 0
+            if n > 100:
+                lens[rng.integers(0, n, 4)] = rng.integers(300, 3000, 4)
+            rows = np.repeat(np.arange(n), lens)
+            cols = rng.integers(0, n, rows.size)
+            vals = rng.uniform(-1, 1, rows.size)
+            rp, col, val = synth.coo_to_csr(n, rows, cols, vals)
+            x = synth.x_vector(n, 7)
+            A = csr(rp, col, val)
+            assert H.spmv_csr(A, x).tobytes() == port.spmv_csr(rp, col, val, x).tobytes(), (variant, n)
+            # theta > 1 selects nothing: an M-HDC with every entry in the remainder
+            m = H.to_mhdc(A, 1.0, 4096)
+            ref = port.to_mhdc(rp, col, val, 1.0, 4096)
+            assert H.spmv_mhdc(m, x).tobytes() == port.spmv_mhdc(ref, x).tobytes(), (variant, n)
+            xd = torch.from_numpy(x).cuda()
+            yd = torch.empty(n, dtype=torch.float64, device="cuda")
+            tiles = torch.empty(m.info.n_tiles, dtype=torch.float64, device="cuda")
+            sc = torch.tensor([0.5], dtype=torch.float64, device="cuda")
+            H.spmv_slab(m, xd.data_ptr(), yd.data_ptr(), 0, m.n_blocks, sc.data_ptr(), tiles.data_ptr())
+            torch.cuda.synchronize()
+            want = port.spmv_mhdc(ref, x * 0.5)
+            assert yd.cpu().numpy().tobytes() == want.tobytes(), (variant, n)
+            assert float(tiles.sum().item()) == pytest.approx(float(np.dot(want, want)), rel=1e-12)
+    finally:
+        H.set_kernel_policy(H.POLICY_AUTO)
