@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 
 // One tiling for both kernels (spmv_kernel and spmv_tma_kernel), so per-tile
 // partial sums and block-range alignment do not depend on which one runs:
-//   <= 8 segments per block (stencil-like) and bl >= 1024, or bl in {128, 256,
+//   <= 32 segments per block (stencil-like) and bl >= 1024, or bl in {128, 256,
 //   512}: 4 rows/thread, 1024-row tiles, ceil(bl/1024) tiles per block (or
 //                         1024/bl whole blocks per tile)
 //   other bl >= 512      : 2 rows/thread, 512-row tiles
@@ -236,7 +236,10 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
     const int64_t t4 = 4 * SPMV_THREADS;
-    if (m.max_seg_per_block <= 8 && (m.bl >= t4 || (m.bl >= 128 && m.bl % 4 == 0 && t4 % m.bl == 0)))
+    // 4 rows/thread up to 32 segments per block: with the interleaved row mapping
+    // config 2 (27 segments) went 90% -> 97% of peak (profiles/r01_v18_r4_c2_ab.log)
+    static const int r4_max_seg = getenv("HDCG_R4_MAXSEG") ? atoi(getenv("HDCG_R4_MAXSEG")) : 32;  // A/B knob
+    if (m.max_seg_per_block <= r4_max_seg && (m.bl >= t4 || (m.bl >= 128 && m.bl % 4 == 0 && t4 % m.bl == 0)))
         t.rows_per_thread = 4;
     else if (m.bl >= 2 * SPMV_THREADS) t.rows_per_thread = 2;
     else t.rows_per_thread = 1;  // incl. bl < 256: 256/bl whole blocks per tile (spmv_blk_kernel)
