@@ -84,7 +84,14 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
         hi = min(lo + a.blocks_per_tile * a.bl, a.n_rows);
     }
     // row of this thread's r-th row
+    // bl = 256 multi-block tiles without a remainder: the TMA kernel's mapping --
+    // lane l of block k's two warps owns block rows 32 (warp & 1) + l + 64 r (per-tile
+    // sums then agree bitwise between the kernels)
+    const bool MBIL = !IL && R == 4 && a.bl == 256 && !a.has_rest;
+    const int warp = threadIdx.x >> 5;
+    const int64_t mb0 = (int64_t)(warp >> 1) * 256 + (warp & 1) * 32 + (threadIdx.x & 31);
     auto row = [&](int r) -> int64_t {
+        if (MBIL) return lo + mb0 + (int64_t)64 * r;
         return IL ? lo + threadIdx.x + (int64_t)SPMV_THREADS * r : lo + (int64_t)R * threadIdx.x + r;
     };
 
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
         const int64_t gi = a.row0 + i0;
         const double* seg_base = a.seg + l;
         constexpr int U = R == 4 ? 4 : SEG_UNROLL;
-        constexpr int64_t RS = IL ? SPMV_THREADS : 1;  // row stride between a thread's rows
+        const int64_t RS = IL ? SPMV_THREADS : MBIL ? 64 : 1;  // row stride between a thread's rows
         for (int k = k0; k < k1; k += U) {
             double v[U][R];
             double xv[U][R];
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                     const double* sp = seg_base + (int64_t)kk * a.bl;
                     // 16-byte loads for consecutive rows unless the slice starts on an
                     // odd slot (odd bl, odd segment index: l is a multiple of R)
-                    if (!IL && R >= 2 && !(kk & a.bl & 1)) {
+                    if (!IL && !MBIL && R >= 2 && !(kk & a.bl & 1)) {
 #pragma unroll
                         for (int h = 0; h < R / 2; ++h) {
                             const double2 t = __ldcs(reinterpret_cast<const double2*>(sp) + h);
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
                 }
             }
         }
-        if (!IL && R >= 2 && a.y_vec_ok && i0 + R - 1 < hi) {
+        if (!IL && !MBIL && R >= 2 && a.y_vec_ok && i0 + R - 1 < hi) {
 #pragma unroll
             for (int h = 0; h < R / 2; ++h)
                 __stcs(reinterpret_cast<double2*>(a.y + i0) + h, make_double2(acc[2 * h], acc[2 * h + 1]));

@@ -342,10 +342,11 @@ __global__ void __launch_bounds__(CONSUMERS, MINB) rest_pipe_kernel(const TmaArg
 // 2 remainder sums already in y (rest_kernel ran first)
 // LAY: tile layout.  0 tiles inside one block, even bl; 1 multi-block tiles
 // (a.blocks_per_tile > 0, R = 4 only); 2 tiles inside one block, odd bl
-// (slices of odd segments start on an odd slot).
+// (slices of odd segments start on an odd slot); 3 multi-block tiles of bl = 256
+// without a remainder, rows interleaved inside each block.
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
 __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
-    constexpr bool MB = LAY == 1;
+    constexpr bool MB = LAY == 1 || LAY == 3;
     constexpr bool ODD = LAY == 2;
     constexpr int TILE = CONSUMERS * R;
     constexpr int STRIDE = ring_stride(R);
@@ -447,16 +448,24 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     // Row mapping: tiles inside one block (LAY 0, 2) are interleaved -- thread t
     // owns tile rows t, t+256, ..., so every x load, shared-memory read and y store
     // of a warp covers 32 consecutive rows (2 L1 wavefronts per 8-byte access
-    // instead of 8 with 4 consecutive rows per thread); multi-block tiles (LAY 1)
-    // keep 4 consecutive rows per thread so that a warp's rows stay in one block.
-    constexpr bool IL = !MB;
+    // instead of 8 with 4 consecutive rows per thread).  Multi-block tiles (LAY 1)
+    // keep 4 consecutive rows per thread (a warp's rows stay in one block), except
+    // bl = 256 without a remainder: there the two warps of a block interleave --
+    // lane l of the block's k-th warp owns block rows 32 k + l + 64 r (87% -> 91%;
+    // the same mapping measured slower for bl = 128 and, with per-run remainder
+    // sums, for bl = 512: profiles/r01_v19_mb_interleaved_ab.log).
+    constexpr bool mbil = LAY == 3;
+    constexpr bool IL = !MB || mbil;
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
     int cs = 0;             // ring stage of the next slice to consume
     uint32_t cphase = 0;    // parity of that stage's current use
     uint32_t par = 0;
-    const int t0 = IL ? (int)threadIdx.x : R * (int)threadIdx.x;  // local row of this thread's first row
-    auto lr = [&](int r) { return IL ? t0 + CONSUMERS * r : t0 + r; };  // local row of its r-th row
+    const int qb = mbil ? warp / 2 : 0;  // bl = 256: this warp's block in the tile
+    // local row of this thread's first row, and the stride between its rows
+    const int t0 = mbil ? qb * 256 + (warp & 1) * 32 + lane : MB ? R * (int)threadIdx.x : (int)threadIdx.x;
+    const int rstride = mbil ? 64 : MB ? 1 : CONSUMERS;
+    auto lr = [&](int r) { return t0 + rstride * r; };  // local row of its r-th row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R, MB>(a, tile);
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? a.y[g.lo + lr(r)] : 0.0;
         } else if constexpr (REST == 1) {
-            if constexpr (IL) {  // the warp's rows are R runs of 32
+            if constexpr (!MB) {  // the warp's rows are R runs of 32
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     const int64_t lo = g.lo + (int64_t)CONSUMERS * r;
@@ -485,7 +494,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
                                         min(lo + CONSUMERS, g.hi), warp, lane, S.scratch + warp * WPASS, a1);
                     acc[r] = a1[0];
                 }
-            } else {
+            } else {  // R consecutive rows per lane (mbil needs REST == 0)
                 warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
                                     S.scratch + warp * WPASS, acc);
             }
@@ -496,7 +505,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         // segment count over the tile's blocks; otherwise kw = k1, the one block's).
         int k0, k1, kw;
         if constexpr (MB) {  // warp-uniform: bl % (32 R) == 0
-            const int64_t bw = (int64_t)g.b + t0 / (int)a.bl;
+            const int64_t bw = (int64_t)g.b + (mbil ? qb : t0 / (int)a.bl);
             const int nbt = (int)min((int64_t)a.blocks_per_tile, a.n_blocks - g.b);
             k0 = bw < a.n_blocks ? __ldg(a.dia_ptr + bw) : 0;
             kw = bw < a.n_blocks ? __ldg(a.dia_ptr + bw + 1) : 0;
@@ -923,7 +932,11 @@ void launch_m(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cu
 template <int R>
 void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if constexpr (R == 4) {
-        if (a.blocks_per_tile > 0) return launch_m<4, 1>(a, grid, smem, scale, norm, st);
+        if (a.blocks_per_tile > 0) {
+            // bl = 256 without a remainder: block-local interleaved rows (tile layout 3)
+            if (a.bl == 256 && !a.has_rest && !a.init_y) return launch_rr<4, 0, 3>(a, grid, smem, scale, norm, st);
+            return launch_m<4, 1>(a, grid, smem, scale, norm, st);
+        }
     }
     if (a.bl % 2) launch_m<R, 2>(a, grid, smem, scale, norm, st);
     else launch_m<R, 0>(a, grid, smem, scale, norm, st);
