@@ -175,6 +175,17 @@ def cpu_model():
     return "unknown"
 
 
+def host_cores():
+    """Widen this thread's CPU mask to the parent's (torchrun's, unbound) and
+    return its size: the reference arm's thread count."""
+    try:
+        mask = os.sched_getaffinity(os.getppid()) | os.sched_getaffinity(0)
+        os.sched_setaffinity(0, mask)
+    except OSError:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
 def run_cpu_reference(workload, fmt, steps, warmup):
     """Times the reference's CPU kernel with all host threads.  Returns a dict."""
     (rp, col, val), bl, sample = cpu_sample(workload)
@@ -188,26 +199,29 @@ def run_cpu_reference(workload, fmt, steps, warmup):
             h = R.csr(rp, col, val)
         else:
             h = R.hdc_handle(rp, col, val, THETA) if fmt == "hdc" else R.mhdc_handle(rp, col, val, THETA, bl)
-        cores = R.max_threads()
+        # every host core, explicitly: under torchrun OMP_NUM_THREADS is 1 (rank 0
+        # alone runs the reference arm) and torch's OpenMP runtime may have bound
+        # this thread to one core; the reference library's runtime inherits the mask
+        cores = host_cores()
 
         y = np.zeros_like(x)
 
         def call():
-            R.spmv(fmt, h, x, out=y)
+            R.spmv(fmt, h, x, workers=cores, out=y)
     except Exception:  # reference library not built: the C port of it
         from oracle.oracle import Port
         P = Port()
         kind = "port"
         m = P.to_hdc(rp, col, val, THETA) if fmt == "hdc" else P.to_mhdc(rp, col, val, THETA, bl)
-        cores = P.max_threads()
+        cores = host_cores()
 
         y = np.zeros_like(x)
 
         def call():
             if fmt == "csr":
-                y[:] = P.spmv_csr(rp, col, val, x, 0)
+                y[:] = P.spmv_csr(rp, col, val, x, cores)
             else:
-                P.spmv_mhdc(m, x, 0, out=y)
+                P.spmv_mhdc(m, x, cores, out=y)
     for _ in range(warmup):
         call()
     times = []
@@ -219,7 +233,7 @@ def run_cpu_reference(workload, fmt, steps, warmup):
     host = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
     if kind == "reference":  # the reference's own membench (bench.cpp:68-110), direct mode, all threads
         try:
-            bps, _ = R.membench(1 << 24, "direct", n_loops=3, n_ites=5)
+            bps, _ = R.membench(1 << 24, "direct", n_loops=3, n_ites=5, workers=cores)
             host["membench_direct_gbs"] = round(bps / 1e9, 2)
         except Exception as e:  # noqa: BLE001 - reported, not fatal
             host["membench_error"] = str(e)
