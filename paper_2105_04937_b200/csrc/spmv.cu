@@ -87,11 +87,12 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
     // bl = 256 multi-block tiles without a remainder: the TMA kernel's mapping --
     // lane l of block k's two warps owns block rows 32 (warp & 1) + l + 64 r (per-tile
     // sums then agree bitwise between the kernels)
-    const bool MBIL = !IL && R == 4 && a.bl == 256 && !a.has_rest;
-    const int warp = threadIdx.x >> 5;
-    const int64_t mb0 = (int64_t)(warp >> 1) * 256 + (warp & 1) * 32 + (threadIdx.x & 31);
+    const bool MBIL = !IL && R == 4 && (a.bl == 256 || a.bl == 128) && !a.has_rest;
+    const int wpb = MBIL ? (int)a.bl / 128 : 1;
+    const int warp = threadIdx.x >> 5, qb = warp / wpb;
+    const int64_t mb0 = (int64_t)qb * a.bl + (warp - qb * wpb) * 32 + (threadIdx.x & 31);
     auto row = [&](int r) -> int64_t {
-        if (MBIL) return lo + mb0 + (int64_t)64 * r;
+        if (MBIL) return lo + mb0 + (int64_t)32 * wpb * r;
         return IL ? lo + threadIdx.x + (int64_t)SPMV_THREADS * r : lo + (int64_t)R * threadIdx.x + r;
     };
 
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
         const int64_t gi = a.row0 + i0;
         const double* seg_base = a.seg + l;
         constexpr int U = R == 4 ? 4 : SEG_UNROLL;
-        const int64_t RS = IL ? SPMV_THREADS : MBIL ? 64 : 1;  // row stride between a thread's rows
+        const int64_t RS = IL ? SPMV_THREADS : MBIL ? 32 * wpb : 1;  // row stride between a thread's rows
         for (int k = k0; k < k1; k += U) {
             double v[U][R];
             double xv[U][R];

@@ -342,11 +342,11 @@ __global__ void __launch_bounds__(CONSUMERS, MINB) rest_pipe_kernel(const TmaArg
 // 2 remainder sums already in y (rest_kernel ran first)
 // LAY: tile layout.  0 tiles inside one block, even bl; 1 multi-block tiles
 // (a.blocks_per_tile > 0, R = 4 only); 2 tiles inside one block, odd bl
-// (slices of odd segments start on an odd slot); 3 multi-block tiles of bl = 256
-// without a remainder, rows interleaved inside each block.
+// (slices of odd segments start on an odd slot); 3 / 4 multi-block tiles of
+// bl = 256 / 128 without a remainder, rows interleaved inside each block.
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
 __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
-    constexpr bool MB = LAY == 1 || LAY == 3;
+    constexpr bool MB = LAY == 1 || LAY == 3 || LAY == 4;
     constexpr bool ODD = LAY == 2;
     constexpr int TILE = CONSUMERS * R;
     constexpr int STRIDE = ring_stride(R);
@@ -450,21 +450,26 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     // of a warp covers 32 consecutive rows (2 L1 wavefronts per 8-byte access
     // instead of 8 with 4 consecutive rows per thread).  Multi-block tiles (LAY 1)
     // keep 4 consecutive rows per thread (a warp's rows stay in one block), except
-    // bl = 256 without a remainder: there the two warps of a block interleave --
-    // lane l of the block's k-th warp owns block rows 32 k + l + 64 r (87% -> 91%;
-    // the same mapping measured slower for bl = 128 and, with per-run remainder
-    // sums, for bl = 512: profiles/r01_v19_mb_interleaved_ab.log).
-    constexpr bool mbil = LAY == 3;
+    // without a remainder for bl = 256 (layout 3: lane l of the block's k-th warp
+    // owns block rows 32 k + l + 64 r; 87% -> 95-97%) and bl = 128 (layout 4: one
+    // warp per block, rows l + 32 r; 83% -> 91%).  Compile-time layouts: with a
+    // runtime warps-per-block, or per-run remainder sums (bl = 512), it was slower
+    // (profiles/r01_v19_*rejected*).
+    constexpr bool mbil = LAY == 3 || LAY == 4;
     constexpr bool IL = !MB || mbil;
     double sc = 1.0;
     if (SCALE) sc = *a.x_scale;
     int cs = 0;             // ring stage of the next slice to consume
     uint32_t cphase = 0;    // parity of that stage's current use
     uint32_t par = 0;
-    const int qb = mbil ? warp / 2 : 0;  // bl = 256: this warp's block in the tile
+    // this warp's block in the tile: two warps per block for bl = 256, one for 128
+    const int qb = LAY == 3 ? warp / 2 : LAY == 4 ? warp : 0;
     // local row of this thread's first row, and the stride between its rows
-    const int t0 = mbil ? qb * 256 + (warp & 1) * 32 + lane : MB ? R * (int)threadIdx.x : (int)threadIdx.x;
-    const int rstride = mbil ? 64 : MB ? 1 : CONSUMERS;
+    const int t0 = LAY == 3   ? qb * 256 + (warp & 1) * 32 + lane
+                   : LAY == 4 ? qb * 128 + lane
+                   : MB       ? R * (int)threadIdx.x
+                              : (int)threadIdx.x;
+    const int rstride = LAY == 3 ? 64 : LAY == 4 ? 32 : MB ? 1 : CONSUMERS;
     auto lr = [&](int r) { return t0 + rstride * r; };  // local row of its r-th row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
@@ -935,6 +940,7 @@ void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cu
         if (a.blocks_per_tile > 0) {
             // bl = 256 without a remainder: block-local interleaved rows (tile layout 3)
             if (a.bl == 256 && !a.has_rest && !a.init_y) return launch_rr<4, 0, 3>(a, grid, smem, scale, norm, st);
+            if (a.bl == 128 && !a.has_rest && !a.init_y) return launch_rr<4, 0, 4>(a, grid, smem, scale, norm, st);
             return launch_m<4, 1>(a, grid, smem, scale, norm, st);
         }
     }

@@ -541,8 +541,8 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
         return ks  # a CSR: the remainder kernel's sums are y
     if blk:
         return ks + [f"hdcg::spmv_blk_kernel<{b(scale)},{b(norm)},{rest}>"]
-    # tile layout: inside one block (0) / multi-block (1; 3 = bl 256 without remainder) / odd bl (2)
-    lay = (3 if info.bl == 256 and info.nnz_rest == 0 else 1) if mb else (2 if info.bl % 2 else 0)
+    # tile layout: inside one block (0) / multi-block (1; without a remainder 3 = bl 256, 4 = bl 128) / odd bl (2)
+    lay = ({256: 3, 128: 4}.get(info.bl, 1) if info.nnz_rest == 0 else 1) if mb else (2 if info.bl % 2 else 0)
     ks.append(f"hdcg::spmv_tma_kernel<{r},{b(scale)},{b(norm)},{rest},{lay}>")
     return ks
 
