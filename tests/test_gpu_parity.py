@@ -536,6 +536,41 @@ def test_kernel_paths_bitwise_identical(port, shape):
         H.set_kernel_policy(H.POLICY_AUTO)
 
 
+@pytest.mark.parametrize("bl", [96, 100, 150, 200])
+def test_blk_tiles_per_stage_block_ranges(port, bl):
+    """spmv_blk_kernel (8 <= bl < 256, whole blocks per tile) over tile-aligned block
+    ranges that split the persistent grid's schedule: y equals the oracle bit for bit,
+    with and without x_scale, with a light remainder (in the kernel) and a heavy one
+    (rest kernel first, init_y)."""
+    rng = np.random.default_rng(23)
+    rp, col, val = synth.laplacian7(36, 30, 28)
+    n = len(rp) - 1
+    heavy = synth.coo_to_csr(n, np.concatenate([np.repeat(np.arange(n), np.diff(rp)), rng.integers(0, n, n)]),
+                             np.concatenate([col.astype(np.int64), rng.integers(0, n, n)]),
+                             np.concatenate([val, rng.uniform(-1, 1, n)]))
+    x = synth.x_vector(n, 9)
+    xd = torch.from_numpy(x).cuda()
+    for (rp2, col2, val2) in ((rp, col, val), heavy):
+        ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
+        m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
+        want = port.spmv_mhdc(ref, x)
+        want_sc = port.spmv_mhdc(ref, x * 0.5)
+        assert H.spmv_mhdc(m, x).tobytes() == want.tobytes(), bl
+        nb = m.n_blocks
+        sc = torch.tensor([0.5], dtype=torch.float64, device="cuda")
+        G = 256 // bl  # blocks per tile: block ranges are tile-aligned
+        for cuts in ((0, 3 * G, nb), (0, 7 * G, 8 * G, 29 * G, G * ((nb - 1) // G), nb), (0, G * (nb // (3 * G)), nb)):
+            y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+            ys = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+            for b0, b1 in zip(cuts[:-1], cuts[1:]):
+                H.spmv_slab(m, xd.data_ptr(), y.data_ptr(), b0, b1)
+                H.spmv_slab(m, xd.data_ptr(), ys.data_ptr(), b0, b1, sc.data_ptr())
+            torch.cuda.synchronize()
+            assert y.cpu().numpy().tobytes() == want.tobytes(), (bl, cuts)
+            assert ys.cpu().numpy().tobytes() == want_sc.tobytes(), (bl, cuts)
+        m.free()
+
+
 def test_tma_policy_rejects_ineligible_shape():
     A = csr(*synth.laplacian7(8, 8, 8))
     m = H.to_mhdc(A, 0.6, 7)
