@@ -571,6 +571,33 @@ def test_blk_tiles_per_stage_block_ranges(port, bl):
         m.free()
 
 
+def test_blk_several_tiles_per_cta(port):
+    """spmv_blk_kernel with several tiles per persistent CTA (64^3 rows, bl = 100 / 50 /
+    10, so the stage ring wraps): the oracle's y bit for bit, with x_scale and the fused
+    per-tile norm, with a light remainder (in the kernel) and a heavy one (summed first)."""
+    rng = np.random.default_rng(31)
+    rp, col, val = synth.laplacian7(64, 64, 64)
+    n = len(rp) - 1
+    heavy = synth.coo_to_csr(n, np.concatenate([np.repeat(np.arange(n), np.diff(rp)), rng.integers(0, n, n)]),
+                             np.concatenate([col.astype(np.int64), rng.integers(0, n, n)]),
+                             np.concatenate([val, rng.uniform(-1, 1, n)]))
+    x = synth.x_vector(n, 5)
+    xd = torch.from_numpy(x).cuda()
+    for (rp2, col2, val2) in ((rp, col, val), heavy):
+        for bl in (100, 50, 10):
+            ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
+            m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
+            assert any("blk" in k for k in H.spmv_kernels(m.info)), bl
+            assert H.spmv_mhdc(m, x).tobytes() == port.spmv_mhdc(ref, x).tobytes(), bl
+            y = torch.empty(n, dtype=torch.float64, device="cuda")
+            tiles = torch.empty(m.info.n_tiles, dtype=torch.float64, device="cuda")
+            sc = torch.tensor([0.5], dtype=torch.float64, device="cuda")
+            H.spmv_slab(m, xd.data_ptr(), y.data_ptr(), 0, m.n_blocks, sc.data_ptr(), tiles.data_ptr())
+            torch.cuda.synchronize()
+            assert y.cpu().numpy().tobytes() == port.spmv_mhdc(ref, x * 0.5).tobytes(), bl
+            m.free()
+
+
 def test_tma_policy_rejects_ineligible_shape():
     A = csr(*synth.laplacian7(8, 8, 8))
     m = H.to_mhdc(A, 0.6, 7)
