@@ -152,11 +152,9 @@ class ClockSampler:
 # CPU reference (bounded sample of the workload)
 
 def cpu_sample(workload):
-    """A bounded sample of the workload, as a standalone CSR the reference can take."""
+    """A bounded sample of the workload, as a standalone CSR the reference can take
+    (configs 1-3; config 4 is timed slab by slab, see run_cpu_reference)."""
     from paper_2105_04937_b200 import synth
-    if workload == "c4":
-        nx, ny, nz = 1024, 1024, 16  # 16 z-planes of config 4: 16.7M rows, same stencil
-        return synth.laplacian7(nx, ny, nz), 4096, f"config-4 z-slab sample {nx}x{ny}x{nz} (16 of 512 planes)"
     if workload == "c1":
         return synth.laplacian7(256, 256, 256), 4096, "config 1 (256^3) in full"
     if workload == "c2":
@@ -164,6 +162,15 @@ def cpu_sample(workload):
     return synth.quasi_diag(1 << 22, seed=4), 8192, "config-3 sample: n = 2^22 (1/4 of the rows)"
 
 
+def c4_slab_samples():
+    """Config 4 as the reference would run it slab by slab: the 32 z-slabs of 16
+    planes (16.7 M rows each) are the first slab (z = 0 Dirichlet face), 30
+    interior slabs that are bitwise the same matrix (constant coefficients, same
+    structure), and the last slab (z = 511 face).  Each sample is the slab's rows
+    with their halo columns, as a square matrix over [z0-1, z1+1) planes whose
+    halo rows are empty (synth.laplacian7_slab_square) -- exactly a rank's work."""
+    nx, ny, nz = GRID4
+    return [(0, 16, 1), (16, 32, 30), (nz - 16, nz, 1)]
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -186,15 +193,15 @@ def host_cores():
     return len(os.sched_getaffinity(0))
 
 
-def run_cpu_reference(workload, fmt, steps, warmup):
-    """Times the reference's CPU kernel with all host threads.  Returns a dict."""
-    (rp, col, val), bl, sample = cpu_sample(workload)
-    x = np.random.default_rng(5).uniform(-1, 1, len(rp) - 1)
-    nnz = int(rp[-1])
+def _reference_timer(rp, col, val, fmt, bl, x, n_loops, warmup):
+    """(seconds per SpMV, kind, cores, handle-keeper) for one sample: the reference's
+    own spmv through its own timing protocol (bench::time_kernel, bench.cpp:44-60:
+    one untimed warm-up loop, then the best per-call average over n_loops loops)
+    with every host thread as `workers`; the C port (oracle/hdc_oracle.c) if the
+    reference library is not built."""
     try:
         from oracle.oracle import Ref
         R = Ref()
-        kind = "reference"
         if fmt == "csr":
             h = R.csr(rp, col, val)
         else:
@@ -203,18 +210,18 @@ def run_cpu_reference(workload, fmt, steps, warmup):
         # alone runs the reference arm) and torch's OpenMP runtime may have bound
         # this thread to one core; the reference library's runtime inherits the mask
         cores = host_cores()
-
-        y = np.zeros_like(x)
-
-        def call():
-            R.spmv(fmt, h, x, workers=cores, out=y)
-    except Exception:  # reference library not built: the C port of it
+        for _ in range(max(0, warmup - 1)):
+            R.spmv(fmt, h, x, workers=cores)
+        best, _ = R.time_spmv(fmt, h, x, workers=cores, n_loops=max(1, n_loops), n_ites=1)
+        return best, "reference", cores, R
+    except Exception as e:  # noqa: BLE001 - reference library not built: the C port of it
+        if "missing" not in str(e):
+            raise
         from oracle.oracle import Port
         P = Port()
-        kind = "port"
-        m = P.to_hdc(rp, col, val, THETA) if fmt == "hdc" else P.to_mhdc(rp, col, val, THETA, bl)
         cores = host_cores()
-
+        m = None if fmt == "csr" else (P.to_hdc(rp, col, val, THETA) if fmt == "hdc"
+                                       else P.to_mhdc(rp, col, val, THETA, bl))
         y = np.zeros_like(x)
 
         def call():
@@ -222,25 +229,67 @@ def run_cpu_reference(workload, fmt, steps, warmup):
                 y[:] = P.spmv_csr(rp, col, val, x, cores)
             else:
                 P.spmv_mhdc(m, x, cores, out=y)
-    for _ in range(warmup):
-        call()
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        call()
-        times.append(time.perf_counter() - t0)
-    t = statistics.mean(times)
+        for _ in range(max(1, warmup)):
+            call()
+        best = float("inf")
+        for _ in range(max(1, n_loops)):
+            t0 = time.perf_counter()
+            call()
+            best = min(best, time.perf_counter() - t0)
+        return best, "port", cores, None
+
+
+def run_cpu_reference(workload, fmt, steps, warmup):
+    """Times the reference's CPU kernel with all host threads.  Returns a dict."""
+    from paper_2105_04937_b200 import synth
     host = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
-    if kind == "reference":  # the reference's own membench (bench.cpp:68-110), direct mode, all threads
+    if workload == "c4":
+        nx, ny, nz = GRID4
+        plane = nx * ny
+        n_full = nx * ny * nz
+        nnz_full = H_gen_laplacian7_nnz(nx, ny, nz)
+        x_full_seed = 5
+        t_total, parts, R = 0.0, [], None
+        for z0, z1, mult in c4_slab_samples():
+            rp, col, val, g0 = synth.laplacian7_slab_square(nx, ny, nz, z0, z1)
+            n_s = len(rp) - 1
+            x = np.zeros(n_s)
+            lo, hi = max(0, g0), min(n_full, g0 + n_s)
+            x[lo - g0:hi - g0] = synth.uniform_pm1(x_full_seed, 0, np.arange(lo, hi, dtype=np.int64))
+            t, kind, cores, R = _reference_timer(rp, col, val, fmt, 4096, x, steps, warmup)
+            t_total += mult * t
+            parts.append(f"z[{z0},{z1}) x{mult}: {t * 1e3:.2f} ms")
+            del rp, col, val, x
+        value = 2.0 * nnz_full / t_total / 1e9
+        sample = ("config 4 slab by slab (16-plane z-slabs with their halo columns, as a rank computes them): "
+                  "first slab, one interior slab (x30: the 30 interior slabs are the same matrix), last slab; "
+                  f"{fmt} theta={THETA} bl=4096; per slab the reference's time_kernel (best of {max(1, steps)} "
+                  f"loops of 1 call after a warm-up loop); whole-matrix SpMV time = sum = {t_total * 1e3:.1f} ms "
+                  f"({'; '.join(parts)}); 2*nnz = {2 * nnz_full}")
+        ms = t_total * 1e3
+        best_ms = ms
+    else:
+        (rp, col, val), bl, sample = cpu_sample(workload)
+        x = np.random.default_rng(5).uniform(-1, 1, len(rp) - 1)
+        nnz = int(rp[-1])
+        t, kind, cores, R = _reference_timer(rp, col, val, fmt, bl, x, steps, warmup)
+        value = 2.0 * nnz / t / 1e9
+        sample = (f"{sample}, {fmt} theta={THETA} bl={bl}, nnz={nnz}, the reference's time_kernel: "
+                  f"best of {max(1, steps)} loops of 1 call ({t * 1e3:.2f} ms) after a warm-up loop")
+        ms = best_ms = t * 1e3
+    if kind == "reference" and R is not None:  # the reference's own membench (bench.cpp:68-110), direct mode
         try:
             bps, _ = R.membench(1 << 24, "direct", n_loops=3, n_ites=5, workers=cores)
             host["membench_direct_gbs"] = round(bps / 1e9, 2)
         except Exception as e:  # noqa: BLE001 - reported, not fatal
             host["membench_error"] = str(e)
-    return {"value": 2.0 * nnz / t / 1e9, "unit": UNIT, "cores": cores, "kind": kind, "host": host,
-            "sample": f"{sample}, {fmt} theta={THETA} bl={bl}, nnz={nnz}, {steps} timed calls "
-                      f"(mean {t * 1e3:.2f} ms) after {warmup} warm-up",
-            "ms_per_call": t * 1e3, "best_ms": min(times) * 1e3}
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "host": host, "sample": sample,
+            "ms_per_call": ms, "best_ms": best_ms}
+
+
+def H_gen_laplacian7_nnz(nx, ny, nz):
+    """nnz of the whole 7-point Dirichlet Laplacian (closed form, no GPU needed)."""
+    return 7 * nx * ny * nz - 2 * (ny * nz + nx * nz + nx * ny)
 
 
 # ---------------------------------------------------------------------------
@@ -258,8 +307,10 @@ def build_config4_slab(H, torch, plan, rank, bl):
     H.gen_laplacian7(nx, ny, nz, z0, z1, rp.data_ptr(), col.data_ptr(), val.data_ptr())
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    # validated like the reference's CsrMatrix constructor (formats.cpp:45-67) on the
+    # device: row pointer shape, column bounds, strictly ascending columns
     m = H.build_mhdc_device(rows, plan.n, row0, nnz, rp.data_ptr(), col.data_ptr(), val.data_ptr(),
-                            THETA, bl, rp64=True, validate=False)
+                            THETA, bl, rp64=True, validate=True)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     del rp, col, val
@@ -271,7 +322,7 @@ def run_ours(a):
     import torch
     import torch.distributed as dist
     from paper_2105_04937_b200 import hdcgpu as H
-    from paper_2105_04937_b200.dist import CudaSlab, PeerHalo, SlabPlan, SlabPowerIteration, verify_halos
+    from paper_2105_04937_b200.dist import CudaSlab, SlabPlan, SlabRunner, all_ranks_agree
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -293,32 +344,19 @@ def run_ours(a):
     info = m.info
 
     # halo transport for N > 1: "p2p" = the boundary SpMVs store their halo rows into
-    # the neighbours' buffers over NVLink (peer memory), "nccl" = send/recv
+    # the neighbours' buffers over NVLink (peer memory), "nccl" = send/recv; the
+    # runner falls back to send/recv on every rank if the peer path fails
     use_p2p = False
     if world > 1 and a.halo != "nccl":
         nbrs = [j for j in (local - 1, local + 1) if 0 <= j < world]
-        can = torch.tensor([int(all(torch.cuda.can_device_access_peer(local, j) for j in nbrs))], device="cuda")
-        dist.all_reduce(can, op=dist.ReduceOp.MIN)
-        use_p2p = bool(can.item())
+        use_p2p = all_ranks_agree(all(torch.cuda.can_device_access_peer(local, j) for j in nbrs), "cuda")
     g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
     compute = CudaSlab(m, halo)
-    pbufs, peer = [], None
 
-    def make_iteration(p2p):
-        nonlocal pbufs, peer
-        if p2p:
-            pbufs = [H.PeerBuffer(rows + 2 * halo) for _ in range(2)]
-            xb, yb = (torch.as_tensor(b, device="cuda") for b in pbufs)
-            peer = PeerHalo(plan, rank, pbufs)
-        else:
-            xb, yb = torch.zeros(rows + 2 * halo, dtype=torch.float64, device="cuda"), None
-        xb.zero_()
-        # x0 = uniform[-1,1] seed 5 over the global rows this slab reads
+    def init_x(xb):  # x0 = uniform[-1,1] seed 5 over the global rows this slab reads
         H.gen_uniform_pm1(5, 0, g0, g1 - g0, xb.data_ptr() + 8 * (g0 - (row0 - halo)))
-        return SlabPowerIteration(plan, rank, compute, xb, comm=world > 1, y_buf=yb, peer=peer)
 
-    it = make_iteration(use_p2p)
-    halo_note = "p2p" if use_p2p else ("nccl" if world > 1 else "none")
+    runner = SlabRunner(plan, rank, compute, init_x, "p2p" if use_p2p else "nccl")
 
     # per-launch kernel events for the roofline (same stream as the kernels)
     kernel_events = []
@@ -331,18 +369,8 @@ def run_ours(a):
         e.record()
         kernel_events.append((s, e))
 
-    for _ in range(a.warmup):
-        it.step()
-    torch.cuda.synchronize()
-    if use_p2p and not verify_halos(plan, rank, it.bufs[0]):
-        # the peer-memory halos did not arrive intact on this box: use NCCL instead
-        it = make_iteration(False)
-        halo_note = "nccl (p2p halo check failed)"
-        for _ in range(a.warmup):
-            it.step()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    runner.warm(a.warmup)
+    it = runner.it
     compute.spmv = timed_spmv
     launches0 = compute.launches
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -359,7 +387,12 @@ def run_ours(a):
     launches = compute.launches - launches0
     ms_local = start.elapsed_time(end) / a.steps
     kern_ms_local = sum(s.elapsed_time(e) for s, e in kernel_events) / a.steps
+    runner.check_after("after_timed")
     norm2 = float(it.red[0].item())
+    y_checksum = runner.y_checksum()
+    bytes_local = b_min(info.dia_slots, info.n_seg, info.n_blocks, info.nnz_rest, rows,
+                        halo_rows=(0 if world == 1 else 2 * halo))
+    ach_local = bytes_local / (kern_ms_local * 1e-3) / 1e9
 
     # ---- e2e through the public host API: H2D x, SpMV, D2H y per step ----------------
     e2e_steps = max(1, min(a.steps, 5))
@@ -389,23 +422,23 @@ def run_ours(a):
         e2e_call()
     e2e_s_local = (time.perf_counter() - t0) / e2e_steps
 
-    # ---- max over ranks -----------------------------------------------------------
-    vec = torch.tensor([ms_local, kern_ms_local, e2e_s_local], dtype=torch.float64, device="cuda")
+    # ---- max over ranks ---------------------------------------------------------
+    vec = torch.tensor([ms_local, kern_ms_local, e2e_s_local, -ach_local], dtype=torch.float64, device="cuda")
     nnz_t = torch.tensor([nnz_local], dtype=torch.int64, device="cuda")
     if world > 1:
         dist.all_reduce(vec, op=dist.ReduceOp.MAX)
         dist.all_reduce(nnz_t, op=dist.ReduceOp.SUM)
-    ms, kern_ms, e2e_s = vec.tolist()
+    ms, kern_ms, e2e_s, neg_ach = vec.tolist()
+    achieved = -neg_ach  # the slowest rank's SpMV bandwidth (its bytes / its kernel time)
     nnz_total = int(nnz_t.item())
+    ok_all = runner.halos_ok_everywhere()
+    halo_note = runner.transport
 
     result = None
     if rank == 0:
         flops = 2.0 * nnz_total
         value = flops / (ms * 1e-3) / 1e9
-        bytes_local = b_min(info.dia_slots, info.n_seg, info.n_blocks, info.nnz_rest, rows,
-                            halo_rows=(0 if world == 1 else 2 * halo))
         peak, peak_kind = load_peaks()
-        achieved = bytes_local / (kern_ms_local * 1e-3) / 1e9
         traffic = load_traffic(f"c4_bl{bl}_n{world}")
         result = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
@@ -417,24 +450,29 @@ def run_ours(a):
                        "n": n, "nnz": nnz_total, "bl": bl, "theta": THETA,
                        "parallelism": f"row-slab x{world} (z-slabs), halo {halo} rows per neighbour"
                                       + {"p2p": ", stored by the boundary SpMV into the neighbours' buffers "
-                                                "(NVLink peer memory, checked after warm-up)",
+                                                "(NVLink peer memory)",
                                          "none": ""}.get(halo_note, f" via {halo_note}"),
                        "l2": "inputs larger than L2 (38.6 GB/step >> 126 MB); no flush needed",
                        "n_seg_rank0": info.n_seg, "nnz_rest_rank0": info.nnz_rest,
-                       "convert_s_rank0": round(t_build, 4)},
+                       "convert_s_rank0": round(t_build, 4), "validated_input": True},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "algorithmic_bytes_per_launch": bytes_local,
-                         "kernel_ms": round(kern_ms_local, 4), "peak_source": f"{peak_kind} hbm_gbs",
+                         "kernel_ms": round(kern_ms, 4), "peak_source": f"{peak_kind} hbm_gbs",
                          "kernel": kernel_name(info, scale=True, norm=True),
+                         "over_ranks": "slowest rank (max kernel time)" if world > 1 else "n/a",
                          "step_share": "SpMV launches = 99.8% of the step's kernel time (profiles/r01_v18_c4_launches.json)"},
             "e2e": {"value": round(flops / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
                     "api": "hdcg_spmv_host (pinned host x/y)" if world == 1 else "per-rank H2D+spmv_slab+D2H"},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "norm2_last": norm2,
+            "result": {"iterations": a.warmup + a.steps, "norm2_last": norm2, "norm2_last_hex": norm2.hex(),
+                       "y_checksum_lo_hi": y_checksum,
+                       "note": "bitwise fingerprint of the final iterate; equal for every N at the same W+K"},
         }
+        if world > 1:
+            result["halo_check"] = {"transport": halo_note, "ok_all_ranks": ok_all, **runner.halo_ok}
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -446,12 +484,7 @@ def run_ours(a):
         print(json.dumps(result), flush=True)
     m.free()
     if world > 1:
-        dist.barrier()
-        if peer is not None:
-            peer.close()
-        dist.barrier()
-        for b in pbufs:
-            b.free()
+        runner.release_peer()
         dist.destroy_process_group()
 
 

@@ -145,6 +145,20 @@ hdcg_status hdcg_get_info(hdcg_matrix m, hdcg_info* info);
 hdcg_status hdcg_export(hdcg_matrix m, int32_t* dia_ptr, int32_t* dia_offsets, double* segments,
                         int32_t* rest_row_ptr, int32_t* rest_col_ind, double* rest_values);
 
+/* The format restricted to the row blocks [block_begin, block_end) -- one slab
+ * of a large matrix, for bit-exact checks of matrices too large to export whole
+ * (config 4: 30 GB of segments).  Same layout as hdcg_export with the block
+ * pointer and the remainder row pointer rebased to 0 at the first block / row:
+ * dia_ptr int32[nb+1], dia_offsets int32[n_seg_range], segments
+ * double[n_seg_range*bl], rest_row_ptr int32[rows+1], rest_col_ind /
+ * rest_values [nnz_rest_range] (columns stay global).  counts (int64[2], may be
+ * NULL) receives {n_seg_range, nnz_rest_range}; any array may be NULL (call
+ * once with NULLs to size them).  No reference counterpart (the reference's
+ * containers expose their vectors directly, formats.hpp:107-132). */
+hdcg_status hdcg_export_blocks(hdcg_matrix m, int64_t block_begin, int64_t block_end, int32_t* dia_ptr,
+                               int32_t* dia_offsets, double* segments, int32_t* rest_row_ptr,
+                               int32_t* rest_col_ind, double* rest_values, int64_t* counts);
+
 /* Replaces hdc::rates(const HdcMatrix&) / rates(const MHdcMatrix&)
  * (convert.hpp:45-52; convert.cpp:173-196), computed on the device from the
  * stored format.  INVALID_ARGUMENT when the matrix holds no nonzeros. */

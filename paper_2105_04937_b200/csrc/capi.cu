@@ -163,8 +163,6 @@ Matrix* unwrap(hdcg_matrix h) {
     return reinterpret_cast<Matrix*>(h);
 }
 
-std::mutex g_host_mu;
-
 }  // namespace
 
 void matrix_release(Matrix* m) {
@@ -179,12 +177,7 @@ void matrix_release(Matrix* m) {
     cudaFree(m->rest_rp);
     cudaFree(m->rest_col);
     cudaFree(m->rest_val);
-    cudaFree(m->dx);
-    cudaFree(m->dy);
-    for (cudaStream_t s : m->pipe)
-        if (s) cudaStreamDestroy(s);
-    for (cudaEvent_t e : m->pipe_events)
-        if (e) cudaEventDestroy(e);
+    for (PipeCtx* c : m->pipe_all) pipe_ctx_release(c);
     cudaSetDevice(prev);
     delete m;
 }
@@ -494,7 +487,7 @@ hdcg_status hdcg_export(hdcg_matrix h, int32_t* dia_ptr, int32_t* dia_offsets, d
                         int32_t* rest_row_ptr, int32_t* rest_col_ind, double* rest_values) {
     return guard([&] {
         const Matrix* m = unwrap(h);
-        HDCG_CUDA(cudaSetDevice(m->device));
+        const DeviceGuard dg(m->device);
         auto cp = [](void* dst, const void* src, size_t bytes) {
             if (dst && src && bytes) HDCG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
         };
@@ -508,10 +501,56 @@ hdcg_status hdcg_export(hdcg_matrix h, int32_t* dia_ptr, int32_t* dia_offsets, d
     });
 }
 
+hdcg_status hdcg_export_blocks(hdcg_matrix h, int64_t block_begin, int64_t block_end, int32_t* dia_ptr,
+                               int32_t* dia_offsets, double* segments, int32_t* rest_row_ptr,
+                               int32_t* rest_col_ind, double* rest_values, int64_t* counts) {
+    return guard([&] {
+        const Matrix* m = unwrap(h);
+        if (block_begin < 0 || block_end > m->n_blocks || block_begin > block_end)
+            fail(HDCG_ERR_INVALID_ARGUMENT, "export_blocks: block range outside the matrix");
+        const DeviceGuard dg(m->device);
+        const int64_t nb = block_end - block_begin;
+        const int64_t r0 = std::min(m->n_rows, block_begin * m->bl), r1 = std::min(m->n_rows, block_end * m->bl);
+        int32_t k[2] = {0, 0}, e[2] = {0, 0};
+        if (m->n_blocks > 0) {
+            HDCG_CUDA(cudaMemcpy(&k[0], m->dia_ptr + block_begin, sizeof(int32_t), cudaMemcpyDeviceToHost));
+            HDCG_CUDA(cudaMemcpy(&k[1], m->dia_ptr + block_end, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        }
+        if (m->rest_rp) {
+            HDCG_CUDA(cudaMemcpy(&e[0], m->rest_rp + r0, sizeof(int32_t), cudaMemcpyDeviceToHost));
+            HDCG_CUDA(cudaMemcpy(&e[1], m->rest_rp + r1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        }
+        if (counts) {
+            counts[0] = k[1] - k[0];
+            counts[1] = e[1] - e[0];
+        }
+        auto cp = [](void* dst, const void* src, size_t bytes) {
+            if (dst && src && bytes) HDCG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+        };
+        if (dia_ptr) {
+            if (m->n_blocks > 0) cp(dia_ptr, m->dia_ptr + block_begin, sizeof(int32_t) * (nb + 1));
+            else dia_ptr[0] = 0;
+            for (int64_t b = 0; b <= nb && m->n_blocks > 0; ++b) dia_ptr[b] -= k[0];
+        }
+        cp(dia_offsets, m->dia_off + k[0], sizeof(int32_t) * (k[1] - k[0]));
+        cp(segments, m->seg + (int64_t)k[0] * m->bl, sizeof(double) * (int64_t)(k[1] - k[0]) * m->bl);
+        if (rest_row_ptr) {
+            if (m->rest_rp) {
+                cp(rest_row_ptr, m->rest_rp + r0, sizeof(int32_t) * (r1 - r0 + 1));
+                for (int64_t i = 0; i <= r1 - r0; ++i) rest_row_ptr[i] -= e[0];
+            } else {
+                for (int64_t i = 0; i <= r1 - r0; ++i) rest_row_ptr[i] = 0;
+            }
+        }
+        cp(rest_col_ind, m->rest_col + e[0], sizeof(int32_t) * (e[1] - e[0]));
+        cp(rest_values, m->rest_val + e[0], sizeof(double) * (e[1] - e[0]));
+    });
+}
+
 hdcg_status hdcg_rates(hdcg_matrix h, double* alpha, double* beta, int64_t* dia_slots) {
     return guard([&] {
         const Matrix* m = unwrap(h);
-        HDCG_CUDA(cudaSetDevice(m->device));
+        const DeviceGuard dg(m->device);
         double a = 0, b = 0;
         int64_t s = 0;
         rates(*m, &a, &b, &s, nullptr);
@@ -539,6 +578,7 @@ hdcg_status hdcg_spmv(hdcg_matrix h, const double* x, double* y, void* stream) {
     return guard([&] {
         const Matrix* m = unwrap(h);
         if (m->n_rows > 0 && (!x || !y)) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: x and y must have length n");
+        const DeviceGuard dg(m->device);
         spmv_launch(*m, x ? x + m->row0 : nullptr, y, 0, m->n_blocks, nullptr, nullptr, (cudaStream_t)stream);
     });
 }
@@ -547,6 +587,7 @@ hdcg_status hdcg_spmv_slab(hdcg_matrix h, const double* x_local, double* y, int6
                            int64_t block_end, const double* x_scale, double* tile_sumsq, void* stream) {
     return guard([&] {
         const Matrix* m = unwrap(h);
+        const DeviceGuard dg(m->device);
         spmv_launch(*m, x_local, y, block_begin, block_end, x_scale, tile_sumsq, (cudaStream_t)stream);
     });
 }
@@ -557,6 +598,7 @@ hdcg_status hdcg_spmv_slab_halo(hdcg_matrix h, const double* x_local, double* y,
     return guard([&] {
         const Matrix* m = unwrap(h);
         if (halo < 0 || halo > m->n_rows) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: halo outside the slab");
+        const DeviceGuard dg(m->device);
         PeerOut p;
         p.lo = peer_lo;
         p.hi = peer_hi;
@@ -606,8 +648,7 @@ hdcg_status hdcg_spmv_host(hdcg_matrix h, const double* x, double* y) {
         Matrix* m = unwrap(h);
         if (m->n_rows == 0) return;
         if (!x || !y) fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: x and y must have length n");
-        std::lock_guard<std::mutex> lock(g_host_mu);
-        spmv_host_pipelined(m, x, y);
+        spmv_host_pipelined(m, x, y);  // per-matrix context pool: concurrent calls allowed
     });
 }
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -34,6 +35,41 @@ inline void cuda_check(cudaError_t e, const char* what) {
 #define HDCG_CUDA(call) ::hdcg::cuda_check((call), #call)
 #define HDCG_LAUNCH_CHECK(name) ::hdcg::cuda_check(cudaGetLastError(), name)
 
+// Makes `dev` current for the lifetime of the guard and restores the caller's
+// device afterwards: every entry point that takes a matrix handle runs on the
+// matrix's device, whatever the calling thread had selected.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        HDCG_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) HDCG_CUDA(cudaSetDevice(dev));
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Per-device one-time state: kernel attributes (max dynamic shared memory) apply
+// to the current device only, so a process that uses matrices on several GPUs
+// configures each kernel once per device.
+inline int current_device_index() {
+    int dev = 0;
+    HDCG_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+struct PerDeviceFlag {
+    uint64_t bits = 0;  // devices 0..63
+    bool test_and_set(int dev) {
+        const uint64_t b = 1ull << (dev & 63);
+        const bool was = (__atomic_fetch_or(&bits, b, __ATOMIC_ACQ_REL) & b) != 0;
+        return was;
+    }
+};
+int sm_count();  // of the current device (cached per device)
+
 // ---- the device-resident matrix -------------------------------------------
 // One storage layout serves M-HDC, HDC (bl = n, one block, lanes) and CSR
 // (no diagonal part):
@@ -55,16 +91,27 @@ struct Matrix {
     int32_t* rest_rp = nullptr;
     int32_t* rest_col = nullptr;
     double* rest_val = nullptr;
-    // lazily allocated state of the host-buffer SpMV pipeline (host_spmv.cu)
-    double* dx = nullptr;
-    double* dy = nullptr;
-    cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
-    std::vector<cudaEvent_t> pipe_events;
-    std::vector<int64_t> chunk_blocks;  // chunk c = blocks [chunk_blocks[c], chunk_blocks[c+1])
+    // lazily built state of the host-buffer SpMV pipeline (host_spmv.cu): the
+    // chunk plan is shared; each concurrent caller borrows its own context
+    // (device x/y buffers, streams, events), so calls on disjoint outputs run
+    // concurrently -- there is no process-wide lock
+    std::mutex pipe_mu;
+    bool pipe_planned = false;
+    std::vector<int64_t> chunk_blocks;  // chunk c = tiles [chunk_blocks[c], chunk_blocks[c+1])
     std::vector<int64_t> chunk_x_hi;    // x entries [0, chunk_x_hi[c]) chunk c reads (global)
     std::vector<int64_t> x_pieces;      // H2D pieces of x: [x_pieces[p], x_pieces[p+1])
+    std::vector<struct PipeCtx*> pipe_free;  // idle contexts
+    std::vector<struct PipeCtx*> pipe_all;   // every context (released with the matrix)
     int64_t device_bytes = 0;
 };
+
+struct PipeCtx {
+    double* dx = nullptr;
+    double* dy = nullptr;
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
+    std::vector<cudaEvent_t> events;
+};
+void pipe_ctx_release(PipeCtx* c);
 
 void matrix_release(Matrix* m);
 

@@ -80,29 +80,75 @@ void plan_pipeline(Matrix* m, cudaStream_t st) {
     const int64_t np = std::max<int64_t>(1, std::min<int64_t>(PIPE_CHUNKS, m->n_cols));
     for (int64_t p = 0; p < np; ++p) m->x_pieces.push_back((m->n_cols * p / np) & ~int64_t(1));
     m->x_pieces.push_back(m->n_cols);
-
-    for (int s = 0; s < 3; ++s) HDCG_CUDA(cudaStreamCreateWithFlags(&m->pipe[s], cudaStreamNonBlocking));
-    m->pipe_events.resize((size_t)(np + n_chunks));
-    for (auto& e : m->pipe_events) HDCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    HDCG_CUDA(cudaMalloc(&m->dx, sizeof(double) * std::max<int64_t>(1, m->n_cols)));
-    HDCG_CUDA(cudaMalloc(&m->dy, sizeof(double) * std::max<int64_t>(1, m->n_rows)));
+    m->pipe_planned = true;
 }
+
+PipeCtx* new_ctx(const Matrix* m) {
+    PipeCtx* c = new PipeCtx();
+    try {
+        for (int s = 0; s < 3; ++s) HDCG_CUDA(cudaStreamCreateWithFlags(&c->s[s], cudaStreamNonBlocking));
+        const size_t ne = m->x_pieces.size() - 1 + m->chunk_blocks.size() - 1;
+        c->events.assign(ne, nullptr);
+        for (auto& e : c->events) HDCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        HDCG_CUDA(cudaMalloc(&c->dx, sizeof(double) * std::max<int64_t>(1, m->n_cols)));
+        HDCG_CUDA(cudaMalloc(&c->dy, sizeof(double) * std::max<int64_t>(1, m->n_rows)));
+    } catch (...) {
+        pipe_ctx_release(c);
+        throw;
+    }
+    return c;
+}
+
+// Borrow an idle pipeline context of m (creating one when every context is busy);
+// returned to the pool when the call ends, also on error.
+struct Borrow {
+    Matrix* m;
+    PipeCtx* c = nullptr;
+    explicit Borrow(Matrix* mm) : m(mm) {
+        std::lock_guard<std::mutex> lock(m->pipe_mu);
+        if (!m->pipe_planned) plan_pipeline(m, nullptr);
+        if (!m->pipe_free.empty()) {
+            c = m->pipe_free.back();
+            m->pipe_free.pop_back();
+        } else {
+            c = new_ctx(m);
+            m->pipe_all.push_back(c);
+        }
+    }
+    ~Borrow() {
+        std::lock_guard<std::mutex> lock(m->pipe_mu);
+        m->pipe_free.push_back(c);
+    }
+};
 
 }  // namespace
 
+void pipe_ctx_release(PipeCtx* c) {
+    if (!c) return;
+    cudaFree(c->dx);
+    cudaFree(c->dy);
+    for (cudaStream_t s : c->s)
+        if (s) cudaStreamDestroy(s);
+    for (cudaEvent_t e : c->events)
+        if (e) cudaEventDestroy(e);
+    delete c;
+}
+
 void spmv_host_pipelined(Matrix* m, const double* x, double* y) {
-    HDCG_CUDA(cudaSetDevice(m->device));
-    if (!m->pipe[0]) plan_pipeline(m, nullptr);
-    cudaStream_t s_in = m->pipe[0], s_k = m->pipe[1], s_out = m->pipe[2];
+    const DeviceGuard dg(m->device);
+    const Borrow b(m);
+    PipeCtx* ctx = b.c;
+    cudaStream_t s_in = ctx->s[0], s_k = ctx->s[1], s_out = ctx->s[2];
     const int64_t np = (int64_t)m->x_pieces.size() - 1;
     const int64_t nc = (int64_t)m->chunk_blocks.size() - 1;
-    cudaEvent_t* ev_in = m->pipe_events.data();
-    cudaEvent_t* ev_k = m->pipe_events.data() + np;
+    cudaEvent_t* ev_in = ctx->events.data();
+    cudaEvent_t* ev_k = ctx->events.data() + np;
     for (int64_t p = 0; p < np; ++p) {
-        const int64_t a = m->x_pieces[p], b = m->x_pieces[p + 1];
-        if (b > a) HDCG_CUDA(cudaMemcpyAsync(m->dx + a, x + a, sizeof(double) * (b - a), cudaMemcpyHostToDevice, s_in));
+        const int64_t a = m->x_pieces[p], e = m->x_pieces[p + 1];
+        if (e > a) HDCG_CUDA(cudaMemcpyAsync(ctx->dx + a, x + a, sizeof(double) * (e - a), cudaMemcpyHostToDevice, s_in));
         HDCG_CUDA(cudaEventRecord(ev_in[p], s_in));
     }
+    const Tiling t = tiling_of(*m);
     int64_t p_done = -1;
     for (int64_t c = 0; c < nc; ++c) {
         // wait for the x pieces up to the one holding column chunk_x_hi[c]-1
@@ -115,16 +161,15 @@ void spmv_host_pipelined(Matrix* m, const double* x, double* y) {
             p_done = p;
         }
         const int64_t q0 = m->chunk_blocks[c], q1 = m->chunk_blocks[c + 1];
-        spmv_launch_tiles(*m, m->dx + m->row0, m->dy, q0, q1, nullptr, nullptr, s_k);
+        spmv_launch_tiles(*m, ctx->dx + m->row0, ctx->dy, q0, q1, nullptr, nullptr, s_k);
         HDCG_CUDA(cudaEventRecord(ev_k[c], s_k));
         HDCG_CUDA(cudaStreamWaitEvent(s_out, ev_k[c], 0));
         int64_t r0, r1, dummy;
-        const Tiling t = tiling_of(*m);
         tile_rows(q0, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &r0, &dummy);
         tile_rows(q1 - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &dummy, &r1);
         r0 = std::min(r0, m->n_rows);
         if (r1 > r0)
-            HDCG_CUDA(cudaMemcpyAsync(y + r0, m->dy + r0, sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost, s_out));
+            HDCG_CUDA(cudaMemcpyAsync(y + r0, ctx->dy + r0, sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost, s_out));
     }
     HDCG_CUDA(cudaStreamSynchronize(s_out));
     HDCG_CUDA(cudaStreamSynchronize(s_in));

@@ -350,7 +350,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     constexpr bool ODD = LAY == 2;
     constexpr int TILE = CONSUMERS * R;
     constexpr int STRIDE = ring_stride(R);
-    constexpr int XG = XGROUP_ROWS / R;  // x registers per thread stay at XGROUP_ROWS doubles
+    // x registers per thread stay at XGROUP_ROWS doubles (8 for the multi-block layout
+    // with consecutive rows per thread, whose wider address math otherwise spills)
+    constexpr int XG = (LAY == 1 || (LAY == 4 && SCALE && NORM) ? XGROUP_ROWS / 2 : XGROUP_ROWS) / R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
     const Smem S = carve(smem_raw, R, NS, a.has_rest);
@@ -368,7 +370,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
 
     if (warp == CONSUMER_WARPS) {
         // ------------------------------ producer ------------------------------
-        if (lane != 0) return;
+        // one lane streams tiles inside a block; multi-block tiles use the whole
+        // warp (lane q issues block q's copies: no per-block register arrays)
+        if (!MB && lane != 0) return;
         const uint64_t policy = evict_first_policy();
         int ps = 0;              // ring stage the next slice goes to
         uint32_t pphase = 0;     // parity of that stage's current use
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
             const Geo g = geo<R, MB>(a, tile);
             if (g.lo >= g.hi) continue;
-            if (a.prefetch) {
+            if (a.prefetch && lane == 0) {
                 if constexpr (REST == 1) {
 #pragma unroll
                     for (int w = 0; w <= CONSUMER_WARPS; ++w)
@@ -387,32 +391,23 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             }
             if constexpr (MB) {
                 // stage j = segment j of each of the tile's blocks, block q's slots at
-                // q*bl (the tile-local row); blocks with fewer segments leave theirs unused
-                constexpr int GMAX = 8;  // TILE / bl <= TILE / (32 R) = 8
+                // q*bl (the tile-local row); blocks with fewer segments leave theirs
+                // unused.  Lane q < G (<= 8) owns block q.
                 const int nbt = (int)min((int64_t)a.blocks_per_tile, a.n_blocks - g.b);
                 const int64_t last_len = min((int64_t)a.bl, a.n_rows - (int64_t)(g.b + nbt - 1) * a.bl);
-                int kst[GMAX], cnt[GMAX];
-                uint32_t pb[GMAX];
-                int J = 0;
-#pragma unroll
-                for (int q = 0; q < GMAX; ++q) {
-                    kst[q] = q < nbt ? __ldg(a.dia_ptr + g.b + q) : 0;
-                    cnt[q] = q < nbt ? __ldg(a.dia_ptr + g.b + q + 1) - kst[q] : 0;
-                    pb[q] = (uint32_t)(((q == nbt - 1 ? last_len : a.bl) + 1) & ~int64_t(1)) * 8u;
-                    J = max(J, cnt[q]);
-                }
-                for (int j = 0; j < J; ++j) {
-                    uint32_t bytes = 0;
-#pragma unroll
-                    for (int q = 0; q < GMAX; ++q)
-                        if (j < cnt[q]) bytes += pb[q];
-                    if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
-                    mbar_expect_tx(&S.full[ps], bytes);
-#pragma unroll
-                    for (int q = 0; q < GMAX; ++q)
-                        if (j < cnt[q])
-                            bulk_g2s(S.ring + ps * STRIDE + q * a.bl, a.seg + (int64_t)(kst[q] + j) * a.bl, pb[q],
-                                     &S.full[ps], policy);
+                const int kst = lane < nbt ? __ldg(a.dia_ptr + g.b + lane) : 0;
+                const int cnt = lane < nbt ? __ldg(a.dia_ptr + g.b + lane + 1) - kst : 0;
+                const uint32_t pb = (uint32_t)(((lane == nbt - 1 ? last_len : a.bl) + 1) & ~int64_t(1)) * 8u;
+                const int J = __reduce_max_sync(0xffffffffu, cnt);
+                const double* src = a.seg + (int64_t)kst * a.bl;
+                for (int j = 0; j < J; ++j, src += a.bl) {
+                    const uint32_t bytes = __reduce_add_sync(0xffffffffu, j < cnt ? pb : 0u);
+                    if (lane == 0) {
+                        if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
+                        mbar_expect_tx(&S.full[ps], bytes);
+                    }
+                    __syncwarp();
+                    if (j < cnt) bulk_g2s(S.ring + ps * STRIDE + lane * a.bl, src, pb, &S.full[ps], policy);
                     if (++ps == NS) {
                         ps = 0;
                         pphase ^= 1u;
@@ -886,11 +881,9 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_blk_kernel(const TmaArgs a, i
 template <bool SCALE, bool NORM, int REST>
 void launch_blk(const TmaArgs& a, int max_seg, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_blk_kernel<SCALE, NORM, REST>;
-    static bool configured = false;
-    if (!configured) {
+    static PerDeviceFlag configured;  // the attribute is per device
+    if (!configured.test_and_set(current_device_index()))
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured = true;
-    }
     k<<<grid, THREADS, smem, st>>>(a, max_seg);
 }
 
@@ -908,11 +901,9 @@ void launch_blk_r(const TmaArgs& a, int max_seg, int grid, size_t smem, bool sca
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM, REST, LAY>;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    static PerDeviceFlag configured;  // per instantiation and device
+    if (!configured.test_and_set(current_device_index()))
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        configured = true;
-    }
     k<<<grid, THREADS, smem, st>>>(a);
 }
 
@@ -948,18 +939,18 @@ void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cu
     else launch_m<R, 0>(a, grid, smem, scale, norm, st);
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
-
 }  // namespace
+
+int sm_count() {
+    static int n[64] = {0};
+    const int dev = current_device_index() & 63;
+    if (!n[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
+    }
+    return n[dev];
+}
 
 bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t tile_begin, int64_t tile_end,
                      const double* x_scale, double* tile_sumsq, cudaStream_t st, const PeerOut& peer) {

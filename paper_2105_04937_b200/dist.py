@@ -88,26 +88,42 @@ class SlabPlan:
 
 
 class HaloExchange:
-    """x halo of a slab buffer laid out as [H left halo | rows owned | H right halo]."""
+    """x halo of a slab buffer laid out as [H left halo | rows owned | H right halo].
+
+    NCCL sends the device slices directly (P2P over NVLink).  Under gloo (the CPU
+    tests, and the one-GPU multi-process test of this code path) a CUDA buffer is
+    staged through host tensors: the boundary rows are copied out, exchanged,
+    and the received halos copied back in wait()."""
 
     def __init__(self, plan: SlabPlan, rank: int):
         self.plan, self.rank = plan, rank
 
     def start(self, buf: torch.Tensor):
         H, rows, r, p = self.plan.halo, self.plan.rows[self.rank], self.rank, self.plan.world
-        ops = []
+        stage = buf.is_cuda and dist.get_backend() == "gloo"
+        pairs = []  # (send slice, recv slice, peer)
         if r > 0:
-            ops.append(dist.P2POp(dist.isend, buf[H:H + H], r - 1))
-            ops.append(dist.P2POp(dist.irecv, buf[0:H], r - 1))
+            pairs.append((buf[H:H + H], buf[0:H], r - 1))
         if r < p - 1:
-            ops.append(dist.P2POp(dist.isend, buf[rows:rows + H], r + 1))
-            ops.append(dist.P2POp(dist.irecv, buf[H + rows:H + rows + H], r + 1))
-        return dist.batch_isend_irecv(ops) if ops else []
+            pairs.append((buf[rows:rows + H], buf[H + rows:H + rows + H], r + 1))
+        ops, back = [], []
+        for snd, rcv, peer in pairs:
+            if stage:
+                s_h, r_h = snd.cpu(), torch.empty(rcv.shape, dtype=rcv.dtype)
+                back.append((rcv, r_h))
+                snd, rcv = s_h, r_h
+            ops.append(dist.P2POp(dist.isend, snd, peer))
+            ops.append(dist.P2POp(dist.irecv, rcv, peer))
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, back
 
     @staticmethod
-    def wait(reqs):
+    def wait(handle):
+        reqs, back = handle
         for q in reqs:
             q.wait()
+        for dst, src in back:  # staged receives (gloo + CUDA buffer)
+            dst.copy_(src)
 
 
 class PeerHalo:
@@ -122,18 +138,22 @@ class PeerHalo:
         self.H, self.plan, self.rank = H, plan, rank
         handles = [b.handle for b in peer_bufs]
         allh = [None] * plan.world
-        dist.all_gather_object(allh, handles)
+        dist.all_gather_object(allh, handles)  # every rank enters it, whatever happens next
         self.mapped, self.lo, self.hi = [], [0, 0], [0, 0]
-        if rank > 0:
-            for i in range(2):
-                base = H.peer_open(allh[rank - 1][i])
-                self.mapped.append(base)
-                self.lo[i] = base + 8 * (plan.halo + plan.rows[rank - 1])
-        if rank < plan.world - 1:
-            for i in range(2):
-                base = H.peer_open(allh[rank + 1][i])
-                self.mapped.append(base)
-                self.hi[i] = base
+        self.error = None
+        try:
+            if rank > 0:
+                for i in range(2):
+                    base = H.peer_open(allh[rank - 1][i])
+                    self.mapped.append(base)
+                    self.lo[i] = base + 8 * (plan.halo + plan.rows[rank - 1])
+            if rank < plan.world - 1:
+                for i in range(2):
+                    base = H.peer_open(allh[rank + 1][i])
+                    self.mapped.append(base)
+                    self.hi[i] = base
+        except Exception as e:  # noqa: BLE001 - reported to the caller, which falls back to NCCL
+            self.error = repr(e)[:160]
 
     def close(self):
         for p in self.mapped:
@@ -214,6 +234,12 @@ class SlabPowerIteration:
         self.halo = HaloExchange(plan, rank)
         self.comm = comm and plan.world > 1
         self.parts, self.interior = plan.boundary_blocks(rank, compute.blocks_per_tile)
+        if self.comm:
+            # every rank's buffers are zeroed before any neighbour's first boundary
+            # SpMV can store halo rows into them (peer mode), or send (NCCL mode)
+            if dev.type == "cuda":
+                torch.cuda.synchronize(dev)
+            dist.barrier()
 
     def step(self):
         x, y = self.bufs
@@ -250,6 +276,122 @@ class SlabPowerIteration:
         self.bufs.reverse()
         self.yi ^= 1
         return self.red
+
+
+def all_ranks_agree(flag: bool, device=None) -> bool:
+    """True on every rank iff `flag` is true on every rank (one tiny all-reduce)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return bool(flag)
+    t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+class SlabRunner:
+    """Builds the power iteration of one rank with a halo transport, checks the
+    halos, and falls back from peer memory to send/recv when the peer path cannot
+    be set up or delivers a wrong halo -- every rank takes the same decision.
+
+    transport: "p2p" (hdcgpu.PeerBuffer + PeerHalo; the boundary SpMVs store the
+    halos), "nccl" (HaloExchange send/recv), "none" (one rank).  init_x(buf) fills
+    the rank's [H | rows | H] x buffer (the halo included)."""
+
+    def __init__(self, plan: SlabPlan, rank: int, compute, init_x, transport: str = "p2p"):
+        self.plan, self.rank, self.compute, self.init_x = plan, rank, compute, init_x
+        self.world = plan.world
+        self.pbufs, self.peer = [], None
+        self.halo_ok = {}
+        self.it, self.transport = None, None
+        if self.world > 1 and transport == "p2p":
+            self.it, self.transport = self._build(True)
+        if self.it is None:
+            note = self.transport
+            self.it, self.transport = self._build(False)
+            if note:
+                self.transport = note
+
+    def _dev(self):
+        return torch.device("cuda", torch.cuda.current_device())
+
+    def release_peer(self):
+        """Unmap the neighbours' buffers on every rank before any rank frees its own."""
+        if self.peer is not None:
+            self.peer.close()
+        self.peer = None
+        if self.world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()
+        for b in self.pbufs:
+            b.free()
+        self.pbufs = []
+
+    def _build(self, p2p: bool):
+        from . import hdcgpu as H
+        rows, halo = self.plan.rows[self.rank], self.plan.halo
+        if p2p:
+            err = ""
+            try:  # local allocation first, agreed on before the collective handle exchange
+                for _ in range(2):
+                    self.pbufs.append(H.PeerBuffer(rows + 2 * halo))
+            except Exception as e:  # noqa: BLE001 - IPC allocation refused on this box
+                err = repr(e)[:120]
+            if all_ranks_agree(not err, self._dev()):
+                self.peer = PeerHalo(self.plan, self.rank, self.pbufs)
+                err = self.peer.error or ""
+                if all_ranks_agree(not err, self._dev()):
+                    err = None
+            if err is not None:
+                self.release_peer()
+                return None, f"nccl (peer-memory setup failed: {err or 'on another rank'})"
+            xb, yb = (torch.as_tensor(b, device="cuda") for b in self.pbufs)
+        else:
+            xb, yb = torch.zeros(rows + 2 * halo, dtype=torch.float64, device="cuda"), None
+        xb.zero_()
+        self.init_x(xb)
+        it = SlabPowerIteration(self.plan, self.rank, self.compute, xb, comm=self.world > 1, y_buf=yb,
+                                peer=self.peer)
+        return it, ("p2p" if p2p else ("nccl" if self.world > 1 else "none"))
+
+    def warm(self, steps: int, force_check_failure: bool = False):
+        """`steps` untimed steps, then the halo check; a failed peer-memory check
+        switches every rank to send/recv and warms that up instead.
+        force_check_failure: treat the p2p check as failed (tests the fallback)."""
+        for _ in range(steps):
+            self.it.step()
+        torch.cuda.synchronize()
+        if self.world == 1:
+            return
+        ok = verify_halos(self.plan, self.rank, self.it.bufs[0])
+        self.halo_ok["after_warmup"] = ok
+        if self.peer is not None and (not all_ranks_agree(ok, self._dev()) or force_check_failure):
+            self.release_peer()
+            self.it, _ = self._build(False)
+            self.transport = "nccl (p2p halo check failed)"
+            for _ in range(steps):
+                self.it.step()
+            torch.cuda.synchronize()
+            self.halo_ok["after_warmup_nccl"] = verify_halos(self.plan, self.rank, self.it.bufs[0])
+        dist.barrier()
+
+    def check_after(self, key: str = "after_timed"):
+        if self.world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()
+            self.halo_ok[key] = verify_halos(self.plan, self.rank, self.it.bufs[0])
+
+    def halos_ok_everywhere(self) -> bool:
+        return all_ranks_agree(all(self.halo_ok.values()), self._dev()) if self.world > 1 else True
+
+    def y_checksum(self):
+        """Sums of the low and high 32-bit halves of the final iterate's bit patterns
+        over every rank's rows (exact in int64 for any partition): equal for every
+        rank count when the sharded y is bitwise the one-GPU y."""
+        halo, rows = self.plan.halo, self.plan.rows[self.rank]
+        yv = self.it.bufs[0][halo:halo + rows].view(torch.int64)
+        ck = torch.stack([(yv & 0xFFFFFFFF).sum(), (yv >> 32).sum()])
+        if self.world > 1:
+            dist.all_reduce(ck, op=dist.ReduceOp.SUM)
+        return [int(v) for v in ck.tolist()]
 
 
 class CudaSlab:

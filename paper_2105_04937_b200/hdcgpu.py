@@ -48,7 +48,7 @@ EXPORTS = (
     "hdcg_export", "hdcg_rates", "hdcg_census", "hdcg_spmv", "hdcg_spmv_host", "hdcg_spmv_slab",
     "hdcg_tree_sum", "hdcg_gen_uniform_pm1", "hdcg_gen_laplacian7", "hdcg_set_kernel_policy",
     "hdcg_membench", "hdcg_analyze", "hdcg_read_matrix_market", "hdcg_spmv_slab_halo",
-    "hdcg_peer_alloc", "hdcg_peer_open", "hdcg_peer_close", "hdcg_peer_free",
+    "hdcg_peer_alloc", "hdcg_peer_open", "hdcg_peer_close", "hdcg_peer_free", "hdcg_export_blocks",
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
@@ -108,6 +108,7 @@ def lib():
         "hdcg_free": [vp],
         "hdcg_get_info": [vp, C.POINTER(Info)],
         "hdcg_export": [vp, vp, vp, vp, vp, vp, vp],
+        "hdcg_export_blocks": [vp, i64, i64, vp, vp, vp, vp, vp, vp, vp],
         "hdcg_rates": [vp, C.POINTER(f64), C.POINTER(f64), C.POINTER(i64)],
         "hdcg_census": [i64, i64, vp, vp, i64, u, vp, vp, vp, C.POINTER(i64)],
         "hdcg_spmv": [vp, vp, vp, vp],
@@ -260,6 +261,26 @@ class DeviceMatrix:
         return out
 
 
+    def export_blocks(self, b0, b1):
+        """The format over row blocks [b0, b1) (hdcg_export_blocks): dia_ptr and the
+        remainder row pointer rebased to 0, columns global."""
+        i = self.info
+        cnt = np.zeros(2, np.int64)
+        check(lib().hdcg_export_blocks(self._h, b0, b1, None, None, None, None, None, None, _ptr(cnt)))
+        rows = min(i.n_rows, b1 * i.bl) - min(i.n_rows, b0 * i.bl)
+        out = dict(
+            dia_ptr=np.zeros(b1 - b0 + 1, np.int32),
+            dia_offsets=np.zeros(cnt[0], np.int32),
+            segments=np.zeros(cnt[0] * i.bl, np.float64),
+            rest_row_ptr=np.zeros(rows + 1, np.int32),
+            rest_col_ind=np.zeros(cnt[1], np.int32),
+            rest_values=np.zeros(cnt[1], np.float64),
+        )
+        check(lib().hdcg_export_blocks(self._h, b0, b1, *[_ptr(out[k]) for k in (
+            "dia_ptr", "dia_offsets", "segments", "rest_row_ptr", "rest_col_ind", "rest_values")], None))
+        return out
+
+
 class MHdcMatrix(DeviceMatrix):
     kind_name = "mhdc"
 
@@ -405,6 +426,12 @@ def _check_plan(plan: BlockPlan, n: int, what: str):
 def _spmv_host(m: DeviceMatrix, x, y, what):
     n = m.n
     x = np.ascontiguousarray(x, dtype=np.float64)
+    if y is not None:
+        # the library writes 8*n bytes through y's pointer: only a writeable,
+        # C-contiguous float64 array of length n may be passed through
+        if not isinstance(y, np.ndarray) or y.dtype != np.float64 or not y.flags.c_contiguous \
+                or not y.flags.writeable or y.ndim != 1:
+            raise ValueError(f"{what}: y must be a writeable, contiguous float64 vector of length n")
     if x.size != n or (y is not None and y.size != n):
         raise ValueError(f"{what}: x and y must have length n")
     out = np.empty(n, np.float64) if y is None else y

@@ -20,9 +20,11 @@
 //
 // Matrices are immutable after construction, so each one is
 // uploaded at most once: a small LRU cache maps a host matrix (its array
-// addresses, sizes and a content fingerprint) to its device handle.  Formats
+// addresses and sizes, verified on every lookup by a hash of every byte of
+// its arrays) to its device handle.  Formats
 // produced by to_hdc / to_mhdc / to_dia are built on the device and
 // registered under the returned object, so their SpMVs never re-upload.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <list>
@@ -30,6 +32,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "hdc/convert.hpp"
@@ -80,46 +83,93 @@ std::vector<index_t> widen(const std::vector<T>& v) {
 }
 
 // ---- device cache -------------------------------------------------------------
+// A host matrix is identified by its array addresses and sizes AND a hash of
+// every byte of its arrays.  The hash is recomputed on every lookup, so a matrix
+// whose storage was freed and reused by another matrix of the same shape (or
+// whose contents were changed in place) never hits a stale device copy: the
+// entry is dropped and the new contents are uploaded.  Hashing reads the arrays
+// once at host memory bandwidth, split over threads -- a fraction of what the
+// PCIe upload it avoids would cost.
 struct Key {
     int kind;
     const void* a;
     const void* b;
     const void* c;
     std::size_t na, nb, nc;
-    uint64_t fp;
     bool operator==(const Key& o) const {
-        return kind == o.kind && a == o.a && b == o.b && c == o.c && na == o.na && nb == o.nb &&
-               nc == o.nc && fp == o.fp;
+        return kind == o.kind && a == o.a && b == o.b && c == o.c && na == o.na && nb == o.nb && nc == o.nc;
     }
 };
 
-uint64_t mix(uint64_t h, uint64_t v) {
+inline uint64_t mix(uint64_t h, uint64_t v) {
     h ^= v + 0x9E3779B97F4A7C15ULL + (h << 6) + (h >> 2);
     return h;
 }
 
-template <class T>
-uint64_t fingerprint(std::span<const T> s, uint64_t h) {
-    // sizes plus a sample of the contents: guards against a freed matrix's
-    // address being reused by a different matrix of the same shape
-    h = mix(h, s.size());
-    const std::size_t n = s.size();
-    const std::size_t step = n > 64 ? n / 64 : 1;
-    for (std::size_t k = 0; k < n; k += step) {
-        uint64_t v = 0;
-        std::memcpy(&v, &s[k], sizeof(T) < 8 ? sizeof(T) : 8);
-        h = mix(h, v);
+inline uint64_t fmix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// 64-bit hash of one chunk of bytes: four independent multiply-rotate lanes
+uint64_t hash_chunk(const unsigned char* p, std::size_t n, uint64_t seed) {
+    uint64_t h[4] = {seed ^ 0x243F6A8885A308D3ULL, seed ^ 0x13198A2E03707344ULL, seed ^ 0xA4093822299F31D0ULL,
+                     seed ^ 0x082EFA98EC4E6C89ULL};
+    constexpr uint64_t P = 0x9FB21C651E98DF25ULL;
+    std::size_t k = 0;
+    for (; k + 32 <= n; k += 32) {
+        uint64_t w[4];
+        std::memcpy(w, p + k, 32);
+        for (int j = 0; j < 4; ++j) {
+            h[j] = (h[j] ^ w[j]) * P;
+            h[j] = (h[j] << 29) | (h[j] >> 35);
+        }
     }
-    if (n) {
-        uint64_t v = 0;
-        std::memcpy(&v, &s[n - 1], sizeof(T) < 8 ? sizeof(T) : 8);
-        h = mix(h, v);
+    uint64_t tail = 0;
+    if (k < n) std::memcpy(&tail, p + k, std::min<std::size_t>(8, n - k));
+    for (std::size_t t = k + 8; t < n; t += 8) {  // <= 3 more words
+        uint64_t w = 0;
+        std::memcpy(&w, p + t, std::min<std::size_t>(8, n - t));
+        tail = fmix(tail ^ w);
     }
+    uint64_t r = fmix(n) ^ fmix(tail);
+    for (int j = 0; j < 4; ++j) r = fmix(r ^ h[j]);
+    return r;
+}
+
+// Whole-array hash: fixed 4 MiB chunks (deterministic for any thread count),
+// hashed in parallel for large arrays, combined in chunk order.
+uint64_t hash_bytes(const void* data, std::size_t n, uint64_t h) {
+    constexpr std::size_t CH = std::size_t(4) << 20;
+    const auto* p = static_cast<const unsigned char*>(data);
+    const std::size_t nch = n == 0 ? 0 : (n + CH - 1) / CH;
+    std::vector<uint64_t> part(nch);
+    auto work = [&](std::size_t c0, std::size_t c1) {
+        for (std::size_t c = c0; c < c1; ++c) part[c] = hash_chunk(p + c * CH, std::min(CH, n - c * CH), c);
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t nt = std::min<std::size_t>(std::min<std::size_t>(hw, 32), nch);
+    if (nt <= 1) {
+        work(0, nch);
+    } else {
+        std::vector<std::thread> th;
+        for (std::size_t t = 0; t < nt; ++t) th.emplace_back(work, nch * t / nt, nch * (t + 1) / nt);
+        for (auto& t : th) t.join();
+    }
+    h = mix(h, n);
+    for (uint64_t v : part) h = mix(h, v);
     return h;
+}
+
+template <class T>
+uint64_t content_hash(std::span<const T> s, uint64_t h) {
+    return hash_bytes(s.data(), s.size_bytes(), h);
 }
 
 struct Entry {
     Key key;
+    uint64_t hash;
     hdcg_matrix h;
     int64_t bytes;
 };
@@ -129,31 +179,51 @@ public:
     ~Cache() {
         for (auto& e : lru_) hdcg_free(e.h);
     }
-    hdcg_matrix find(const Key& k) {
+    // the device copy of (key, hash); an entry at the same key with a different
+    // hash (storage reused or contents changed) is freed
+    hdcg_matrix find(const Key& k, uint64_t hash) {
         std::lock_guard<std::mutex> lock(mu_);
         for (auto it = lru_.begin(); it != lru_.end(); ++it)
             if (it->key == k) {
-                lru_.splice(lru_.begin(), lru_, it);
-                return it->h;
+                if (it->hash == hash) {
+                    lru_.splice(lru_.begin(), lru_, it);
+                    return it->h;
+                }
+                bytes_ -= it->bytes;
+                hdcg_free(it->h);
+                lru_.erase(it);
+                return nullptr;
             }
         return nullptr;
     }
-    void put(const Key& k, hdcg_matrix h) {
+    void put(const Key& k, uint64_t hash, hdcg_matrix h) {
         hdcg_info info{};
         hdcg_get_info(h, &info);
         std::lock_guard<std::mutex> lock(mu_);
-        lru_.push_front(Entry{k, h, info.device_bytes});
+        for (auto it = lru_.begin(); it != lru_.end(); ++it)
+            if (it->key == k) {  // superseded
+                bytes_ -= it->bytes;
+                hdcg_free(it->h);
+                lru_.erase(it);
+                break;
+            }
+        lru_.push_front(Entry{k, hash, h, info.device_bytes});
         bytes_ += info.device_bytes;
+        // the newest entry always stays (its caller is about to use it)
         while (lru_.size() > 1 && (lru_.size() > kMaxEntries || bytes_ > kMaxBytes)) {
             bytes_ -= lru_.back().bytes;
             hdcg_free(lru_.back().h);
             lru_.pop_back();
         }
     }
+    std::size_t size() {
+        std::lock_guard<std::mutex> lock(mu_);
+        return lru_.size();
+    }
 
 private:
-    static constexpr std::size_t kMaxEntries = 256;
-    static constexpr int64_t kMaxBytes = int64_t(64) << 30;
+    static constexpr std::size_t kMaxEntries = 64;
+    static constexpr int64_t kMaxBytes = int64_t(8) << 30;  // retained HBM beyond the newest entry
     std::mutex mu_;
     std::list<Entry> lru_;
     int64_t bytes_ = 0;
@@ -166,35 +236,41 @@ Cache& cache() {
 
 enum { K_CSR = 1, K_DIA = 2, K_HDC = 3, K_MHDC = 4 };
 
-Key key_of(const CsrMatrix& m) {
-    uint64_t fp = fingerprint(m.values(), fingerprint(m.col_ind(), fingerprint(m.row_ptr(), m.n())));
-    return Key{K_CSR, m.values().data(), m.col_ind().data(), m.row_ptr().data(), m.values().size(),
-               m.col_ind().size(), m.row_ptr().size(), fp};
+struct Ident {
+    Key key;
+    uint64_t hash;
+};
+
+Ident ident(const CsrMatrix& m) {
+    const uint64_t h = content_hash(m.values(), content_hash(m.col_ind(), content_hash(m.row_ptr(), m.n())));
+    return {Key{K_CSR, m.values().data(), m.col_ind().data(), m.row_ptr().data(), m.values().size(),
+                m.col_ind().size(), m.row_ptr().size()},
+            h};
 }
-Key key_of(const DiaMatrix& m) {
-    uint64_t fp = fingerprint(m.lanes(), fingerprint(m.offsets(), m.n()));
-    return Key{K_DIA, m.lanes().data(), m.offsets().data(), nullptr, m.lanes().size(), m.offsets().size(), 0, fp};
+Ident ident(const DiaMatrix& m) {
+    const uint64_t h = content_hash(m.lanes(), content_hash(m.offsets(), m.n()));
+    return {Key{K_DIA, m.lanes().data(), m.offsets().data(), nullptr, m.lanes().size(), m.offsets().size(), 0}, h};
 }
-Key key_of(const HdcMatrix& m) {
-    Key d = key_of(m.dia());
-    Key c = key_of(m.csr());
-    return Key{K_HDC, d.a, d.b, c.a, d.na, d.nb, c.na, mix(d.fp, c.fp)};
+Ident ident(const HdcMatrix& m) {
+    const Ident d = ident(m.dia()), c = ident(m.csr());
+    return {Key{K_HDC, d.key.a, d.key.b, c.key.a, d.key.na, d.key.nb, c.key.na}, mix(d.hash, c.hash)};
 }
-Key key_of(const MHdcMatrix& m) {
-    uint64_t fp = fingerprint(m.segments(), fingerprint(m.dia_offsets(), fingerprint(m.dia_ptr(), m.bl())));
-    Key c = key_of(m.csr());
-    return Key{K_MHDC, m.segments().data(), m.dia_offsets().data(), c.a, m.segments().size(),
-               m.dia_offsets().size(), c.na, mix(fp, c.fp)};
+Ident ident(const MHdcMatrix& m) {
+    const uint64_t h = content_hash(m.segments(), content_hash(m.dia_offsets(), content_hash(m.dia_ptr(), m.bl())));
+    const Ident c = ident(m.csr());
+    return {Key{K_MHDC, m.segments().data(), m.dia_offsets().data(), c.key.a, m.segments().size(),
+                m.dia_offsets().size(), c.key.na},
+            mix(h, c.hash)};
 }
 
 hdcg_matrix device_of(const CsrMatrix& m) {
-    const Key k = key_of(m);
-    if (hdcg_matrix h = cache().find(k)) return h;
+    const Ident id = ident(m);
+    if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     const I32View rp(m.row_ptr()), col(m.col_ind());
     hdcg_matrix h = nullptr;
     call(hdcg_build_csr(m.n(), static_cast<int64_t>(m.values().size()), rp.ptr, col.ptr, m.values().data(), 0,
                         nullptr, &h));
-    cache().put(k, h);
+    cache().put(id.key, id.hash, h);
     return h;
 }
 
@@ -215,29 +291,29 @@ hdcg_matrix upload_hdc(index_t n, std::span<const index_t> offsets, std::span<co
 }
 
 hdcg_matrix device_of(const DiaMatrix& m) {
-    const Key k = key_of(m);
-    if (hdcg_matrix h = cache().find(k)) return h;
+    const Ident id = ident(m);
+    if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     hdcg_matrix h = upload_hdc(m.n(), m.offsets(), m.lanes(), nullptr);
-    cache().put(k, h);
+    cache().put(id.key, id.hash, h);
     return h;
 }
 
 hdcg_matrix device_of(const HdcMatrix& m) {
-    const Key k = key_of(m);
-    if (hdcg_matrix h = cache().find(k)) return h;
+    const Ident id = ident(m);
+    if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     hdcg_matrix h = upload_hdc(m.n(), m.dia().offsets(), m.dia().lanes(), &m.csr());
-    cache().put(k, h);
+    cache().put(id.key, id.hash, h);
     return h;
 }
 
 hdcg_matrix device_of(const MHdcMatrix& m) {
-    const Key k = key_of(m);
-    if (hdcg_matrix h = cache().find(k)) return h;
+    const Ident id = ident(m);
+    if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     const I32View dp(m.dia_ptr()), offs(m.dia_offsets()), rp(m.csr().row_ptr()), col(m.csr().col_ind());
     hdcg_matrix h = nullptr;
     call(hdcg_upload_mhdc(m.n(), m.bl(), dp.ptr, m.n_segments(), offs.ptr, m.segments().data(), rp.ptr,
                           static_cast<int64_t>(m.csr().values().size()), col.ptr, m.csr().values().data(), 0, &h));
-    cache().put(k, h);
+    cache().put(id.key, id.hash, h);
     return h;
 }
 
@@ -346,7 +422,8 @@ DiaMatrix to_dia(const CsrMatrix& m) {
     hdcg_matrix h = build_hdc_device(m, 0.0);  // theta = 0: every populated diagonal is a lane
     Exported e = export_all(h);
     DiaMatrix d(m.n(), widen(e.offsets), std::move(e.segments));
-    cache().put(key_of(d), h);
+    const Ident id = ident(d);
+    cache().put(id.key, id.hash, h);
     return d;
 }
 
@@ -356,7 +433,8 @@ HdcMatrix to_hdc(const CsrMatrix& m, real_t theta) {
     Exported e = export_all(h);
     HdcMatrix out(m.n(), DiaMatrix(m.n(), widen(e.offsets), std::move(e.segments)),
                   CsrMatrix(m.n(), std::move(e.rest_val), widen(e.rest_col), widen(e.rest_rp)), theta);
-    cache().put(key_of(out), h);
+    const Ident id = ident(out);
+    cache().put(id.key, id.hash, h);
     return out;
 }
 
@@ -370,7 +448,8 @@ MHdcMatrix to_mhdc(const CsrMatrix& m, real_t theta, index_t bl) {
     Exported e = export_all(h);
     MHdcMatrix out(m.n(), bl, widen(e.dia_ptr), widen(e.offsets), std::move(e.segments),
                    CsrMatrix(m.n(), std::move(e.rest_val), widen(e.rest_col), widen(e.rest_rp)), theta);
-    cache().put(key_of(out), h);
+    const Ident id = ident(out);
+    cache().put(id.key, id.hash, h);
     return out;
 }
 

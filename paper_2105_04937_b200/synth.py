@@ -102,6 +102,25 @@ def laplacian7(nx: int, ny: int, nz: int, z0: int = 0, z1: int | None = None):
     return _csr_from_slots(cols, vals, present)
 
 
+def laplacian7_slab_square(nx: int, ny: int, nz: int, z0: int, z1: int):
+    """The rows of z-planes [z0, z1) of the 7-point Laplacian with everything they
+    read, as a SQUARE matrix over the planes [z0-1, z1+1): the halo planes' rows
+    are empty, columns are shifted by g0 = (z0-1)*nx*ny.  Its middle rows are the
+    slab's rows exactly (same entries, same order; M-HDC blocks of any bl dividing
+    nx*ny are the global blocks), so a square-matrix library (the reference) can
+    compute one rank's slab of config 4.  Returns (rp, col, val, g0)."""
+    p = nx * ny
+    rp_s, col_s, val_s = laplacian7(nx, ny, nz, z0, z1)
+    g0 = (z0 - 1) * p
+    n = (z1 - z0 + 2) * p
+    rp = np.empty(n + 1, dtype=np.int64)
+    rp[:p] = 0
+    rp[p:p + rp_s.size] = rp_s
+    rp[p + rp_s.size:] = rp_s[-1]
+    col = (col_s.astype(np.int64) - g0).astype(np.int32)
+    return rp, col, val_s, g0
+
+
 # ---------------------------------------------------------------------------
 # config 2: 27-point stencil, off-diagonals uniform[-1,0) (stream 1), diag 1 + sum|off|
 

@@ -1,0 +1,164 @@
+// shim_cache_test.cpp -- the GPU shim's device cache must never serve a stale
+// device copy through the reference's C++ API.
+//
+// Linked like acceptance_gpu (oracle/Makefile target `shim`): the reference's
+// formats.cpp (containers) + paper_2105_04937_b200/shim/hdc_gpu_shim.cpp +
+// libhdcgpu.so.  Three hazards, each checked against a plain host loop in the
+// reference's per-row order (remainder first, then segments ascending;
+// proj/src/kernels.cpp:173-206), bit for bit:
+//   1. a matrix whose contents change in place (same addresses and sizes), one
+//      value at a position a sampled fingerprint would skip;
+//   2. a matrix destroyed and a same-shape matrix with one different value
+//      constructed (storage usually reused by the allocator);
+//   3. the same for a CSR through spmv_csr.
+// Exit code 0 = all pass; prints the failing case otherwise.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "hdc/convert.hpp"
+#include "hdc/formats.hpp"
+#include "hdc/kernels.hpp"
+
+using namespace hdc;
+
+namespace {
+
+std::vector<real_t> host_mhdc(const MHdcMatrix& m, const std::vector<real_t>& x) {
+    const index_t n = m.n(), bl = m.bl();
+    std::vector<real_t> y(n, 0.0);
+    auto rp = m.csr().row_ptr();
+    auto ci = m.csr().col_ind();
+    auto cv = m.csr().values();
+    for (index_t i = 0; i < n; ++i) {
+        real_t s = 0.0;
+        for (index_t k = rp[i]; k < rp[i + 1]; ++k) s += cv[k] * x[ci[k]];
+        y[i] = s;
+    }
+    auto dp = m.dia_ptr();
+    auto off = m.dia_offsets();
+    auto seg = m.segments();
+    for (index_t b = 0; b < m.n_blocks(); ++b) {
+        const index_t r0 = b * bl, r1 = std::min(n, r0 + bl);
+        for (index_t k = dp[b]; k < dp[b + 1]; ++k)
+            for (index_t i = std::max(r0, -off[k]); i < std::min(r1, n - off[k]); ++i)
+                y[i] += seg[(size_t)k * bl + (i - r0)] * x[i + off[k]];
+    }
+    return y;
+}
+
+std::vector<real_t> host_csr(const CsrMatrix& m, const std::vector<real_t>& x) {
+    std::vector<real_t> y(m.n(), 0.0);
+    auto rp = m.row_ptr();
+    for (index_t i = 0; i < m.n(); ++i) {
+        real_t s = 0.0;
+        for (index_t k = rp[i]; k < rp[i + 1]; ++k) s += m.values()[k] * x[m.col_ind()[k]];
+        y[i] = s;
+    }
+    return y;
+}
+
+bool same(const std::vector<real_t>& a, const std::vector<real_t>& b) {
+    return a.size() == b.size() && std::memcmp(a.data(), b.data(), sizeof(real_t) * a.size()) == 0;
+}
+
+// banded test matrix: offsets -3, -1, 0, 2, 700 where in range, plus a sparse tail
+CsrMatrix make_csr(index_t n, double bump) {
+    std::vector<real_t> v;
+    std::vector<index_t> c, rp{0};
+    for (index_t i = 0; i < n; ++i) {
+        for (index_t o : {-3, -1, 0, 2, 700, 5000 + (i % 7)}) {
+            const index_t j = i + o;
+            if (j < 0 || j >= n) continue;
+            if (o >= 5000 && i % 5) continue;
+            c.push_back(j);
+            v.push_back(1.0 + 0.001 * ((i * 31 + j * 17) % 97) + (i == n / 3 && o == 0 ? bump : 0.0));
+        }
+        rp.push_back((index_t)v.size());
+    }
+    return CsrMatrix(n, std::move(v), std::move(c), std::move(rp));
+}
+
+int fails = 0;
+void expect(bool ok, const char* what) {
+    std::printf("%s: %s\n", ok ? "ok  " : "FAIL", what);
+    if (!ok) ++fails;
+}
+
+}  // namespace
+
+int main() {
+    const index_t n = 200003, bl = 1000;
+    std::vector<real_t> x(n);
+    for (index_t i = 0; i < n; ++i) x[i] = 1.0 / (1.0 + (i % 1013));
+
+    // 1. in-place change of one segment value (same addresses, same sizes)
+    {
+        MHdcMatrix a = to_mhdc(make_csr(n, 0.0), 0.6, bl);
+        std::vector<real_t> y(n);
+        spmv_mhdc(a, x, y);
+        expect(same(y, host_mhdc(a, x)), "to_mhdc result, first call");
+        auto seg = a.segments();
+        const size_t pos = seg.size() / 2 + 12345 % 997 + 1;  // off any 1/64 sampling grid
+        real_t* p = const_cast<real_t*>(seg.data()) + pos;
+        const real_t old = *p;
+        *p = old + 0.5;
+        spmv_mhdc(a, x, y);
+        expect(same(y, host_mhdc(a, x)), "segment value changed in place");
+        *p = old;
+        spmv_mhdc(a, x, y);
+        expect(same(y, host_mhdc(a, x)), "segment value restored in place");
+        auto rv = a.csr().values();
+        if (!rv.empty()) {
+            real_t* q = const_cast<real_t*>(rv.data()) + rv.size() / 3 + 7;
+            *q += 0.25;
+            spmv_mhdc(a, x, y);
+            expect(same(y, host_mhdc(a, x)), "remainder value changed in place");
+        }
+    }
+    // 2. destroy / re-create a same-shape matrix with one value different
+    {
+        const void* prev_seg = nullptr;
+        std::vector<real_t> prev_y;
+        for (int round = 0; round < 4; ++round) {
+            MHdcMatrix m = to_mhdc(make_csr(n, 0.0), 0.6, bl);
+            // a foreign matrix (not produced by to_mhdc), built from copies of m's arrays
+            std::vector<index_t> dp(m.dia_ptr().begin(), m.dia_ptr().end());
+            std::vector<index_t> of(m.dia_offsets().begin(), m.dia_offsets().end());
+            std::vector<real_t> sg(m.segments().begin(), m.segments().end());
+            sg[sg.size() / 2 + 321] += 0.125 * round;
+            CsrMatrix rest(n, std::vector<real_t>(m.csr().values().begin(), m.csr().values().end()),
+                           std::vector<index_t>(m.csr().col_ind().begin(), m.csr().col_ind().end()),
+                           std::vector<index_t>(m.csr().row_ptr().begin(), m.csr().row_ptr().end()));
+            MHdcMatrix f(n, bl, std::move(dp), std::move(of), std::move(sg), std::move(rest), 0.6);
+            std::vector<real_t> y(n);
+            spmv_mhdc(f, x, y);
+            const bool reused = f.segments().data() == prev_seg;
+            char what[160];
+            std::snprintf(what, sizeof what, "re-created foreign M-HDC, round %d (storage %s)", round,
+                          reused ? "reused" : "new");
+            expect(same(y, host_mhdc(f, x)), what);
+            if (round > 0) expect(!same(y, prev_y), "re-created matrix differs from the previous one");
+            prev_seg = f.segments().data();
+            prev_y = y;
+        }
+    }
+    // 3. CSR through spmv_csr, changed in place and re-created
+    {
+        CsrMatrix c = make_csr(n, 0.0);
+        std::vector<real_t> y(n);
+        spmv_csr(c, x, y);
+        expect(same(y, host_csr(c, x)), "spmv_csr first call");
+        real_t* q = const_cast<real_t*>(c.values().data()) + c.values().size() / 2 + 77;
+        *q *= 3.0;
+        spmv_csr(c, x, y);
+        expect(same(y, host_csr(c, x)), "spmv_csr after in-place change");
+        for (int round = 1; round < 3; ++round) {
+            CsrMatrix d = make_csr(n, 0.5 * round);
+            spmv_csr(d, x, y);
+            expect(same(y, host_csr(d, x)), "spmv_csr re-created with a changed diagonal value");
+        }
+    }
+    std::printf(fails ? "shim cache test: %d failure(s)\n" : "shim cache test: all passed\n", fails);
+    return fails ? 1 : 0;
+}

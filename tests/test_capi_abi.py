@@ -71,3 +71,23 @@ def test_host_side_validation():
     assert (p.n_blocks, p.begin(2), p.end(2), p.length(2)) == (3, 8, 10, 2)
     assert hdcgpu.BlockPlan.rows(0, 4).n_blocks == 0
     assert hdcgpu.BlockPlan.rows(3, 100).end(0) == 3
+
+
+def test_host_spmv_rejects_unsafe_y():
+    """The library writes 8*n bytes through y's pointer: float32, strided, read-only
+    or wrong-length outputs are rejected before any device call (ValueError, like
+    the reference's length check, kernels.cpp:21-24)."""
+    class Fake:  # a matrix handle of 4 rows; never reaches the library
+        n = 4
+        handle = None
+
+    x = np.ones(4)
+    bad = [np.zeros(4, np.float32), np.zeros(8)[::2], np.zeros(5), np.zeros((2, 2)), [0.0] * 4]
+    ro = np.zeros(4)
+    ro.flags.writeable = False
+    bad.append(ro)
+    for y in bad:
+        with pytest.raises(ValueError):
+            hdcgpu._spmv_host(Fake(), x, y, "spmv_mhdc")
+    with pytest.raises(ValueError):
+        hdcgpu._spmv_host(Fake(), np.ones(3), None, "spmv_mhdc")

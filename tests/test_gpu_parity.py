@@ -629,6 +629,20 @@ def test_reference_acceptance_through_gpu_shim():
     assert "all 8 criteria passed" in r.stdout
 
 
+CACHE_TEST = os.path.join(os.path.dirname(ACCEPT), "shim_cache_test")
+
+
+@pytest.mark.skipif(not os.path.exists(CACHE_TEST), reason="shim_cache_test not built (needs /root/reference)")
+def test_shim_cache_never_serves_stale_matrices():
+    """tests/cpp/shim_cache_test.cpp through the reference's C++ API: matrices changed
+    in place at unsampled positions, destroyed and re-created at reused addresses,
+    CSR and M-HDC -- y bitwise equal to a host loop in the reference's order."""
+    r = subprocess.run([CACHE_TEST], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(CACHE_TEST))
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all passed" in r.stdout
+
+
 @pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT])
 def test_remainder_paths(port, rest_mode):
     """The TMA kernel's ways of summing the CSR remainder (consumers load it from
@@ -823,10 +837,10 @@ def test_matrix_market_large_parallel_parse(tmp_path, port):
 # ---------------------------------------------------------------------------
 # peer-memory halo (the p2p transport of dist.py), two processes on one GPU
 
-def _peer_halo_worker(rank, world, port, nx, ny, nz, bl, steps, out_dir):
+def _peer_halo_worker(rank, world, port, nx, ny, nz, bl, steps, out_dir, transport="p2p"):
     import torch.distributed as dist
 
-    from paper_2105_04937_b200.dist import CudaSlab, PeerHalo, SlabPlan, SlabPowerIteration, verify_halos
+    from paper_2105_04937_b200.dist import CudaSlab, SlabPlan, SlabRunner
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -841,47 +855,61 @@ def _peer_halo_worker(rank, world, port, nx, ny, nz, bl, steps, out_dir):
     d_val = torch.empty(nnz, dtype=torch.float64, device="cuda")
     H.gen_laplacian7(nx, ny, nz, z0, z1, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr())
     m = H.build_mhdc_device(rows, n, row0, nnz, d_rp.data_ptr(), d_col.data_ptr(), d_val.data_ptr(), 0.6, bl)
-    pbufs = [H.PeerBuffer(rows + 2 * halo) for _ in range(2)]
-    xb, yb = (torch.as_tensor(b, device="cuda") for b in pbufs)
-    xb.zero_()
     g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
-    H.gen_uniform_pm1(5, 0, g0, g1 - g0, xb.data_ptr() + 8 * (g0 - (row0 - halo)))
-    peer = PeerHalo(plan, rank, pbufs) if world > 1 else None
-    it = SlabPowerIteration(plan, rank, CudaSlab(m, halo), xb, comm=world > 1, y_buf=yb, peer=peer)
-    for _ in range(steps):
-        it.step()
-    torch.cuda.synchronize()
-    ok = verify_halos(plan, rank, it.bufs[0]) if world > 1 else True
+
+    def init_x(xb):
+        H.gen_uniform_pm1(5, 0, g0, g1 - g0, xb.data_ptr() + 8 * (g0 - (row0 - halo)))
+
+    # p2p: peer-memory halos; sendrecv: dist.HaloExchange (NCCL send/recv in
+    # production, gloo staged through host buffers here); p2p_fallback: the p2p
+    # check is forced to fail after the warm-up and every rank switches to send/recv
+    runner = SlabRunner(plan, rank, CudaSlab(m, halo), init_x, "nccl" if transport == "sendrecv" else "p2p")
+    runner.warm(2, force_check_failure=transport == "p2p_fallback")
+    for _ in range(steps - 2):
+        runner.it.step()
+    runner.check_after("after")
+    ok = runner.halos_ok_everywhere()
+    ck = runner.y_checksum()
+    it = runner.it
     np.save(os.path.join(out_dir, f"y{world}_{rank}.npy"), it.bufs[0][halo:halo + rows].cpu().numpy())
     np.save(os.path.join(out_dir, f"red{world}_{rank}.npy"), it.red.cpu().numpy())
     np.save(os.path.join(out_dir, f"ok{world}_{rank}.npy"), np.array([ok]))
-    dist.barrier()
-    if peer is not None:
-        peer.close()
+    np.save(os.path.join(out_dir, f"ck{world}_{rank}.npy"), np.array(ck, np.int64))
+    with open(os.path.join(out_dir, f"tr{world}_{rank}.txt"), "w") as f:
+        f.write(runner.transport)
+    runner.release_peer()
     dist.destroy_process_group()
 
 
-def test_peer_halo_power_iteration_two_processes(tmp_path):
-    """dist.py's p2p transport: two ranks (processes sharing this GPU through CUDA
-    IPC mappings) run the config-4 power iteration on z-slabs; the boundary SpMVs
-    store their halo rows straight into the neighbour's buffers.  y and ||y|| are
-    bitwise those of one rank, and the halos hold exactly the neighbours' rows."""
+@pytest.mark.parametrize("transport", ["p2p", "sendrecv", "p2p_fallback"])
+def test_peer_halo_power_iteration_two_processes(tmp_path, transport):
+    """dist.py's halo transports with the real CUDA kernel, two ranks as processes
+    sharing this GPU: p2p -- the boundary SpMVs store their halo rows straight into
+    the neighbour's buffers (CUDA IPC mappings); sendrecv -- dist.HaloExchange
+    (NCCL send/recv in production, gloo staged through host buffers here),
+    overlapped with the interior blocks; p2p_fallback -- the p2p halo check forced
+    to fail, every rank switching to send/recv (bench.py's fallback).  y, ||y|| and
+    the y checksum are bitwise those of one rank; the halos hold exactly the
+    neighbours' rows after the warm-up and at the end."""
     import socket
 
     import torch.multiprocessing as mp
-    nx, ny, nz, bl, steps = 32, 32, 16, 256, 4
+    nx, ny, nz, bl, steps = 32, 32, 16, 256, 5
     for world in (1, 2):
         with socket.socket() as s:
             s.bind(("127.0.0.1", 0))
             port = s.getsockname()[1]
-        mp.spawn(_peer_halo_worker, args=(world, port, nx, ny, nz, bl, steps, str(tmp_path)), nprocs=world,
-                 join=True)
+        mp.spawn(_peer_halo_worker, args=(world, port, nx, ny, nz, bl, steps, str(tmp_path), transport),
+                 nprocs=world, join=True)
     y1 = np.load(tmp_path / "y1_0.npy")
     y2 = np.concatenate([np.load(tmp_path / f"y2_{r}.npy") for r in range(2)])
     assert y2.tobytes() == y1.tobytes()
     for r in range(2):
         assert np.load(tmp_path / f"red2_{r}.npy").tobytes() == np.load(tmp_path / "red1_0.npy").tobytes()
         assert bool(np.load(tmp_path / f"ok2_{r}.npy")[0])
+        assert np.array_equal(np.load(tmp_path / f"ck2_{r}.npy"), np.load(tmp_path / "ck1_0.npy"))
+    tr = (tmp_path / "tr2_0.txt").read_text()
+    assert tr == {"p2p": "p2p", "sendrecv": "nccl", "p2p_fallback": "nccl (p2p halo check failed)"}[transport]
 
 
 @pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
