@@ -245,7 +245,8 @@ hdcg_status hdcg_peer_free(void* ptr);
  * kernel only, 2 TMA kernel only (ineligible shapes then fail with
  * INVALID_ARGUMENT); policy >> 4 = how the TMA kernel reads the CSR remainder:
  * 0 default, 1 consumers load it from global memory, 2 a separate kernel sums
- * it into y first.  All produce
+ * it into y first, 3 gather warps of the same kernel sum it into shared memory
+ * for the tiles ahead of the consumers (matrices with segments).  All produce
  * bitwise identical y and tile sums; this exists for testing. */
 hdcg_status hdcg_set_kernel_policy(int policy);
 

@@ -679,8 +679,8 @@ hdcg_status hdcg_membench(int64_t n, int mode, int n_loops, int n_ites, double* 
 
 hdcg_status hdcg_set_kernel_policy(int policy) {
     return guard([&] {
-        if (policy < 0 || (policy & 3) > 2 || (policy & 0xC) != 0 || (policy >> 4) > 2)
-            fail(HDCG_ERR_INVALID_ARGUMENT, "kernel policy must be (0, 1 or 2) + 16 * (0, 1 or 2)");
+        if (policy < 0 || (policy & 3) > 2 || (policy & 0xC) != 0 || (policy >> 4) > 3)
+            fail(HDCG_ERR_INVALID_ARGUMENT, "kernel policy must be (0, 1 or 2) + 16 * (0, 1, 2 or 3)");
         g_kernel_policy = policy & 3;
         g_rest_mode = policy >> 4;
     });

@@ -49,6 +49,13 @@ constexpr int CONSUMERS = CONSUMER_WARPS * 32;
 constexpr int THREADS = CONSUMERS + 32;  // + producer warp
 constexpr int XGROUP_ROWS = 16;          // x values loaded ahead per thread (segments x rows)
 constexpr int WPASS = 256;               // remainder scratch per warp (entries per pass <= this)
+// fused remainder mode (REST == 3): gather warps sum the CSR remainder of the
+// tiles ahead into shared memory while the consumers stream segments
+constexpr int GATHER_WARPS = 4;
+constexpr int GPER = 8;                  // x gathers per lane per pass
+constexpr int GPASS = 32 * GPER;         // entries per gather-warp pass
+constexpr int RS_BUFS = 3;               // tiles of remainder sums in flight
+__host__ __device__ constexpr int gather_rows_per_warp(int R) { return 256 * R / GATHER_WARPS; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -123,6 +130,7 @@ struct TmaArgs {
     double* peer_hi;
     int64_t halo;
     int prefetch;  // producer prefetches the consumers' tile-start lines into L2
+    int fused;     // REST == 3: remainder sums by the gather warps (shared memory)
 };
 
 struct Geo {
@@ -153,27 +161,48 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
 __host__ __device__ constexpr int ring_stride(int R) { return CONSUMERS * R + 2; }
 
 // has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
-__host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest) {
-    return sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
-                             2 * CONSUMER_WARPS) +
-           sizeof(uint64_t) * (2 * nstage);
+// fused: the gather warps' remainder sums (RS_BUFS tiles), scratch and row pointers
+__host__ __device__ inline size_t fused_int_bytes(int R) {
+    return ((size_t)GATHER_WARPS * (gather_rows_per_warp(R) + 1) * sizeof(int32_t) + 15) & ~size_t(15);
+}
+__host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest, int fused = 0) {
+    size_t b = sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
+                                 2 * CONSUMER_WARPS) +
+               sizeof(uint64_t) * (2 * nstage);
+    if (fused)
+        b += sizeof(double) * ((size_t)RS_BUFS * CONSUMERS * R + GATHER_WARPS * GPASS) + fused_int_bytes(R) +
+             sizeof(uint64_t) * 2 * RS_BUFS;
+    return b;
 }
 
 struct Smem {
     double* ring;     // nstage * ring_stride(R)
     double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
     double* wsum;     // 2 * CONSUMER_WARPS (fused norm: double-buffered warp partials)
+    double* rsum;     // fused: RS_BUFS * TILE remainder sums, tile-local rows
+    double* gscratch; // fused: GATHER_WARPS * GPASS products
+    int32_t* grp;     // fused: GATHER_WARPS * (rows per gather warp + 1) row pointers
     uint64_t* full;
     uint64_t* empty;
+    uint64_t* rs_full;   // fused: a tile's sums are ready (GATHER_WARPS arrivals)
+    uint64_t* rs_empty;  // fused: the consumers have read them (CONSUMER_WARPS arrivals)
 };
 
-__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int has_rest) {
+__device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, int has_rest, int fused = 0) {
     Smem s;
     s.ring = reinterpret_cast<double*>(base);
     s.scratch = s.ring + (size_t)nstage * ring_stride(R);
     s.wsum = s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0);
-    s.full = reinterpret_cast<uint64_t*>(s.wsum + 2 * CONSUMER_WARPS);
+    double* d = s.wsum + 2 * CONSUMER_WARPS;
+    s.rsum = d;
+    s.gscratch = d + (fused ? RS_BUFS * CONSUMERS * R : 0);
+    d = s.gscratch + (fused ? GATHER_WARPS * GPASS : 0);
+    s.grp = reinterpret_cast<int32_t*>(d);
+    unsigned char* u = reinterpret_cast<unsigned char*>(d) + (fused ? fused_int_bytes(R) : 0);
+    s.full = reinterpret_cast<uint64_t*>(u);
     s.empty = s.full + nstage;
+    s.rs_full = s.empty + nstage;
+    s.rs_empty = s.rs_full + RS_BUFS;
     return s;
 }
 
@@ -338,24 +367,99 @@ __global__ void __launch_bounds__(CONSUMERS, MINB) rest_pipe_kernel(const TmaArg
     } while (c < e1);
 }
 
+// One gather warp's rows [w0, w0 + nrows) of a tile (nrows <= 32 * G): the
+// remainder sums in stored order onto +0.0 (kernels.cpp:192-197), written to
+// out[0 .. nrows) in shared memory.  rest_pipe_kernel's pipeline: the warp's row
+// pointers staged once, the entry range walked in passes of GPASS entries with
+// the next pass's columns loaded while this pass's x gathers and values are in
+// flight, products through the warp's scratch, each lane adding its row's
+// products in order.  Bitwise equal to warp_rest / rest_pipe_kernel.
+template <bool SCALE, int G>
+__device__ __forceinline__ void gather_rest_rows(const TmaArgs& a, int64_t w0, int nrows, double sc, double* scratch,
+                                                 int32_t* rps, double* out, int lane) {
+    constexpr int WROWS = 32 * G;
+    for (int i = lane; i <= WROWS; i += 32) rps[i] = __ldg(a.rest_rp + w0 + min(i, nrows));
+    __syncwarp();
+    const int e0 = rps[0], e1 = rps[WROWS];
+    int g = 0;
+    int kb = rps[lane], ke = rps[lane + 1];
+    int gend = rps[32];
+    double acc = 0.0;
+    int32_t cn[GPER];
+#pragma unroll
+    for (int j = 0; j < GPER; ++j) {
+        const int q = e0 + lane + 32 * j;
+        cn[j] = q < e1 ? __ldcs(a.rest_col + q) : 0;
+    }
+    int c = e0;
+    do {
+        int32_t cl[GPER];
+        double xl[GPER], vl[GPER];
+#pragma unroll
+        for (int j = 0; j < GPER; ++j) cl[j] = cn[j];
+#pragma unroll
+        for (int j = 0; j < GPER; ++j) {
+            const int q = c + lane + 32 * j;
+            xl[j] = q < e1 ? __ldg(a.x + ((int64_t)cl[j] - a.row0)) : 0.0;
+            vl[j] = q < e1 ? __ldcs(a.rest_val + q) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < GPER; ++j) {
+            const int q = c + GPASS + lane + 32 * j;
+            cn[j] = q < e1 ? __ldcs(a.rest_col + q) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < GPER; ++j) {
+            double xv = xl[j];
+            if (SCALE) xv = __dmul_rn(xv, sc);
+            scratch[lane + 32 * j] = __dmul_rn(vl[j], xv);
+        }
+        __syncwarp();
+        const int cend = c + GPASS;
+        while (true) {
+            const int p0 = max(kb, c), p1 = min(ke, cend);
+            for (int p = p0; p < p1; ++p) acc = __dadd_rn(acc, scratch[p - c]);
+            if (gend > cend || g >= G) break;  // the run continues in the next pass
+            const int r = 32 * g + lane;
+            if (r < nrows) out[r] = acc;
+            acc = 0.0;
+            if (++g >= G || 32 * g >= nrows) {
+                g = G;
+                break;
+            }
+            kb = rps[32 * g + lane];
+            ke = rps[32 * g + lane + 1];
+            gend = rps[min(32 * g + 32, WROWS)];
+        }
+        __syncwarp();
+        c = cend;
+    } while (c < e1);
+    // rows of runs the pass loop never reached (no entries left): +0.0
+    for (int r = 32 * g + lane; r < nrows; r += 32) out[r] = 0.0;
+}
+
 // REST: 0 no remainder, 1 remainder summed here from global memory (fused),
 // 2 remainder sums already in y (rest_kernel ran first)
 // LAY: tile layout.  0 tiles inside one block, even bl; 1 multi-block tiles
 // (a.blocks_per_tile > 0, R = 4 only); 2 tiles inside one block, odd bl
 // (slices of odd segments start on an odd slot); 3 / 4 multi-block tiles of
 // bl = 256 / 128 without a remainder, rows interleaved inside each block.
+// REST == 3 (fused): warps 9 .. 9+GATHER_WARPS-1 are gather warps (remainder
+// sums of the tiles ahead into shared memory, RS_BUFS tiles in flight); the
+// consumers start each row from its sum.  Two CTAs per SM.
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
-__global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
+__global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS, REST == 3 ? 2 : 3)
+    spmv_tma_kernel(const TmaArgs a) {
     constexpr bool MB = LAY == 1 || LAY == 3 || LAY == 4;
     constexpr bool ODD = LAY == 2;
     constexpr int TILE = CONSUMERS * R;
     constexpr int STRIDE = ring_stride(R);
     // x registers per thread stay at XGROUP_ROWS doubles (8 for the multi-block layout
     // with consecutive rows per thread, whose wider address math otherwise spills)
-    constexpr int XG = (LAY == 1 || (LAY == 4 && SCALE && NORM) ? XGROUP_ROWS / 2 : XGROUP_ROWS) / R;
+    constexpr int XG = (LAY == 1 || (SCALE && NORM && (LAY == 4 || REST == 3)) ? XGROUP_ROWS / 2 : XGROUP_ROWS) / R;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int NS = a.nstage;
-    const Smem S = carve(smem_raw, R, NS, a.has_rest);
+    const Smem S = carve(smem_raw, R, NS, a.has_rest, REST == 3);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -364,9 +468,47 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
             mbar_init(&S.full[s], 1);
             mbar_init(&S.empty[s], CONSUMER_WARPS);
         }
+        if (REST == 3) {
+            for (int s = 0; s < RS_BUFS; ++s) {
+                mbar_init(&S.rs_full[s], GATHER_WARPS);
+                mbar_init(&S.rs_empty[s], CONSUMER_WARPS);
+            }
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+
+    if constexpr (REST == 3) {
+        if (warp > CONSUMER_WARPS) {
+            // -------------------------- gather warps --------------------------
+            constexpr int GROWS = gather_rows_per_warp(R);
+            const int gw = warp - CONSUMER_WARPS - 1;
+            double* scratch = S.gscratch + gw * GPASS;
+            int32_t* rps = S.grp + gw * (GROWS + 1);
+            const double sc = SCALE ? *a.x_scale : 1.0;
+            int rb = 0;
+            uint32_t rph = 0;
+            bool wrapped = false;
+            for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
+                const Geo g = geo<R, MB>(a, tile);
+                if (g.lo >= g.hi) continue;  // the consumers skip it too
+                if (wrapped) mbar_wait(&S.rs_empty[rb], rph ^ 1u);
+                const int64_t w0 = g.lo + (int64_t)gw * GROWS;
+                const int nrows = (int)max((int64_t)0, min((int64_t)GROWS, g.hi - w0));
+                if (nrows > 0)
+                    gather_rest_rows<SCALE, GROWS / 32>(a, w0, nrows, sc, scratch, rps,
+                                                        S.rsum + rb * (CONSUMERS * R) + gw * GROWS, lane);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&S.rs_full[rb]);
+                if (++rb == RS_BUFS) {
+                    rb = 0;
+                    rph ^= 1u;
+                    wrapped = true;
+                }
+            }
+            return;
+        }
+    }
 
     if (warp == CONSUMER_WARPS) {
         // ------------------------------ producer ------------------------------
@@ -467,6 +609,8 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
     const int rstride = LAY == 3 ? 64 : LAY == 4 ? 32 : MB ? 1 : CONSUMERS;
     auto lr = [&](int r) { return t0 + rstride * r; };  // local row of its r-th row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
+    int rb = 0;          // REST == 3: remainder-sum buffer of this tile
+    uint32_t rph = 0;
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R, MB>(a, tile);
         if (g.lo >= g.hi) {
@@ -478,9 +622,24 @@ __global__ void __launch_bounds__(THREADS, 3) spmv_tma_kernel(const TmaArgs a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-        // CSR remainder first (stored order).  Either fused here (few remainder
-        // entries) or already summed into y by rest_kernel (remainder-heavy matrices).
-        if constexpr (REST == 2) {
+        // CSR remainder first (stored order).  Fused here (few remainder entries),
+        // already summed into y by rest_kernel (REST 2), or summed by this CTA's
+        // gather warps into shared memory (REST 3, remainder-heavy matrices).
+        if constexpr (REST == 3) {
+            mbar_wait(&S.rs_full[rb], rph);
+            const double* rs = S.rsum + rb * (CONSUMERS * R);
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? rs[lr(r)] : 0.0;
+            // release the buffer once the sums are in registers
+#pragma unroll
+            for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.rs_empty[rb]);
+            if (++rb == RS_BUFS) {
+                rb = 0;
+                rph ^= 1u;
+            }
+        } else if constexpr (REST == 2) {
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? a.y[g.lo + lr(r)] : 0.0;
         } else if constexpr (REST == 1) {
@@ -904,7 +1063,8 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     static PerDeviceFlag configured;  // per instantiation and device
     if (!configured.test_and_set(current_device_index()))
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    k<<<grid, THREADS, smem, st>>>(a);
+    constexpr int threads = REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS;
+    k<<<grid, threads, smem, st>>>(a);
 }
 
 template <int R, int REST, int LAY>
@@ -920,7 +1080,8 @@ void launch_rr(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, c
 
 template <int R, int LAY>
 void launch_m(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
-    if (a.init_y) launch_rr<R, 2, LAY>(a, grid, smem, scale, norm, st);
+    if (a.fused) launch_rr<R, 3, LAY>(a, grid, smem, scale, norm, st);
+    else if (a.init_y) launch_rr<R, 2, LAY>(a, grid, smem, scale, norm, st);
     else if (a.has_rest) launch_rr<R, 1, LAY>(a, grid, smem, scale, norm, st);
     else launch_rr<R, 0, LAY>(a, grid, smem, scale, norm, st);
 }
@@ -930,8 +1091,9 @@ void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cu
     if constexpr (R == 4) {
         if (a.blocks_per_tile > 0) {
             // bl = 256 without a remainder: block-local interleaved rows (tile layout 3)
-            if (a.bl == 256 && !a.has_rest && !a.init_y) return launch_rr<4, 0, 3>(a, grid, smem, scale, norm, st);
-            if (a.bl == 128 && !a.has_rest && !a.init_y) return launch_rr<4, 0, 4>(a, grid, smem, scale, norm, st);
+            const bool plain = !a.has_rest && !a.init_y && !a.fused;
+            if (a.bl == 256 && plain) return launch_rr<4, 0, 3>(a, grid, smem, scale, norm, st);
+            if (a.bl == 128 && plain) return launch_rr<4, 0, 4>(a, grid, smem, scale, norm, st);
             return launch_m<4, 1>(a, grid, smem, scale, norm, st);
         }
     }
@@ -1000,14 +1162,21 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         a.prefetch = e ? atoi(e) : (t.blocks_per_tile > 0 ? 1 : 0);
     }
     // Remainder mode (hdcg_set_kernel_policy / HDCG_REST_MODE override the default):
-    // 2 summed first by rest_kernel -- the default for remainder-heavy matrices (>= 1
-    // entry per 4 rows); 1 loaded from global memory by the consumers -- the default
-    // otherwise.  (A third mode, the producer staging the remainder through the
-    // ring, measured 33% at config 3 and was removed: profiles/README.md.)
+    // 3 summed by the CTA's gather warps into shared memory, tiles ahead of the
+    // consumers -- the default for remainder-heavy matrices (>= 1 entry per 4 rows)
+    // with segments; 2 summed first into y by rest_pipe_kernel -- the default for a
+    // CSR (no segments); 1 loaded from global memory by the consumers -- the
+    // default otherwise.  (A producer staging the remainder through the ring
+    // measured 33% at config 3 and was removed: profiles/README.md.)
     static const int env_mode = getenv("HDCG_REST_MODE") ? atoi(getenv("HDCG_REST_MODE")) : 0;
     const int req = g_rest_mode ? g_rest_mode : env_mode;
-    const int mode = req >= 1 && req <= 2 ? req : (m.nnz_rest * 4 >= m.n_rows ? 2 : 1);
+    const bool heavy = m.nnz_rest * 4 >= m.n_rows;
+    const bool fusable = !blk && m.n_seg > 0;
+    int mode = req >= 1 && req <= 3 ? req : (heavy ? (fusable ? 3 : 2) : 1);
+    if (mode == 3 && !fusable) mode = 2;
     const bool split = a.has_rest && mode == 2;
+    a.fused = a.has_rest && mode == 3;
+    if (a.fused) a.has_rest = 0;  // no consumer scratch: the gather warps own the remainder
     auto rest_rows = [&](int64_t tb, int64_t te, cudaStream_t s) {
         // rows covered by the tile range (tiles are contiguous in rows)
         int64_t r0, r1, dummy;
@@ -1050,6 +1219,7 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     static const int env_kb = getenv("HDCG_TMA_STAGE_KB") ? atoi(getenv("HDCG_TMA_STAGE_KB")) : 0;
     static const int env_ctas = getenv("HDCG_TMA_CTAS") ? atoi(getenv("HDCG_TMA_CTAS")) : 0;
     auto tma = [&](const TmaArgs& base, int64_t tb, int64_t te, int want_ctas, cudaStream_t s) {
+        // (REST 3 needs one CTA's gather warps and consumers on the same tiles: any grid works)
         TmaArgs b = base;
         b.tile_begin = (int)tb;
         b.tile_end = (int)te;
@@ -1078,11 +1248,12 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
             HDCG_LAUNCH_CHECK("spmv_blk_kernel");
             return;
         }
+        if (b.fused) want_ctas = std::min(want_ctas, 2);  // 13 warps per CTA: 2 per SM
         const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
-        const size_t fixed = smem_bytes(R, 0, b.has_rest);
+        const size_t fixed = smem_bytes(R, 0, b.has_rest, b.fused);
         const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
         b.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
-        const size_t smem = smem_bytes(R, b.nstage, b.has_rest);
+        const size_t smem = smem_bytes(R, b.nstage, b.has_rest, b.fused);
         const int fit = (int)((227 * 1024) / (smem + 1024));
         const int per_sm = std::max(1, std::min(want_ctas, fit));
         const int64_t cap = (int64_t)sm_count() * per_sm;

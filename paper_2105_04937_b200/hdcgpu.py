@@ -52,7 +52,7 @@ EXPORTS = (
 )
 
 POLICY_AUTO, POLICY_GENERAL, POLICY_TMA = 0, 1, 2
-REST_DEFAULT, REST_GLOBAL, REST_SPLIT = 0, 1, 2
+REST_DEFAULT, REST_GLOBAL, REST_SPLIT, REST_FUSED = 0, 1, 2, 3
 
 
 class LibraryMissing(ImportError):
@@ -563,6 +563,8 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     if not ((info.bl >= 256 and inside) or mb or blk):
         return [f"hdcg::spmv_kernel<{r},{b(scale)},{b(norm)}>"]
     rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
+    if rest == 2 and info.n_seg > 0 and not blk:
+        rest = 3  # gather warps inside the segment kernel
     ks = ["hdcg::rest_pipe_kernel"] if rest == 2 else []
     if rest == 2 and info.n_seg == 0 and not norm:
         return ks  # a CSR: the remainder kernel's sums are y
@@ -636,5 +638,5 @@ def membench(n: int, mode: str = "direct", n_loops: int = 20, n_ites: int = 1000
 def set_kernel_policy(policy: int, rest_mode: int = 0):
     """policy: 0 auto (TMA kernel where eligible), 1 general kernel only, 2 TMA kernel only.
     rest_mode (TMA kernel's CSR remainder): 0 default, 1 global loads, 2 summed first
-    by a separate kernel."""
+    by a separate kernel, 3 summed by gather warps of the same kernel (shared memory)."""
     check(lib().hdcg_set_kernel_policy(policy + 16 * rest_mode))

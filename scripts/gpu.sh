@@ -14,6 +14,7 @@
 #   ncu:NAME:REGEX:SKIP:ARGS   the bench command plain, then ncu --set full of the
 #                              first launch of kernels matching REGEX after SKIP
 #   py:NAME:SCRIPT:ARGS        python SCRIPT ARGS > NAME.log
+#   env:VAR=VALUE / unenv:VAR  set / clear an environment variable for the later steps
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 TAG=$1; shift
 O=gpurun_out/$TAG
@@ -40,6 +41,8 @@ for step in "$@"; do
          timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:$a2" -s "$a3" -c 1 \
              -o "$O/$a1" $CMD > "$O/$a1.ncu.log" 2>&1
          st "ncu_$a1" $? ;;
+    env) export "$a1"; echo "env $a1" >> "$O/status.txt" ;;
+    unenv) unset "$a1"; echo "unenv $a1" >> "$O/status.txt" ;;
     py) timeout 1200 python "$a2" ${a3//,/ } > "$O/$a1.log" 2>&1; st "py_$a1" $? ;;
     *) st "unknown_$step" 1 ;;
   esac

@@ -334,7 +334,7 @@ def test_config3_quasi_diagonal(port):
         assert y.tobytes() == want.tobytes()
         assert_within_tol(y, yc, rp, col, val, x)
         try:  # every remainder mode at scale
-            for mode in (H.REST_GLOBAL, H.REST_SPLIT):
+            for mode in (H.REST_GLOBAL, H.REST_SPLIT, H.REST_FUSED):
                 H.set_kernel_policy(H.POLICY_TMA, mode)
                 for _ in range(3):
                     assert H.spmv_mhdc(m, x).tobytes() == want.tobytes(), (bl, mode)
@@ -643,7 +643,7 @@ def test_shim_cache_never_serves_stale_matrices():
     assert "all passed" in r.stdout
 
 
-@pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT])
+@pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT, H.REST_FUSED])
 def test_remainder_paths(port, rest_mode):
     """The TMA kernel's ways of summing the CSR remainder (consumers load it from
     global memory; a separate rest_kernel sums it into y first)

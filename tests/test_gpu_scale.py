@@ -113,7 +113,7 @@ def test_config3_full_size(gold):
             assert digest(e[arr], dt) == d[arr], (key, arr)
         assert list(H.rates(m)) == [d["rates"][0], d["rates"][1], d["rates"][2]], key
         try:
-            for mode in (H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT):
+            for mode in (H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT, H.REST_FUSED):
                 H.set_kernel_policy(H.POLICY_AUTO, mode)
                 y = H.spmv_mhdc(m, x)
                 assert y[:4].tolist() == d["y_head"], (key, mode)
