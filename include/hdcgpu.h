@@ -69,10 +69,13 @@ typedef struct {
     int64_t dia_slots;  /* rates().dia_slots: segments x true block lengths */
     int64_t nnz_input;  /* stored entries of the original CSR (2*nnz flops / SpMV) */
     int64_t n_tiles;    /* SpMV tiles (one sum-of-squares partial each) */
-    int64_t tile_rows;  /* rows per tile (tiles never straddle a block) */
-    int64_t blocks_per_tile; /* >1 when bl < tile_rows */
+    int64_t tile_rows;  /* rows per tile (tiles never straddle a block, except packed tiles) */
+    int64_t blocks_per_tile; /* block-range granularity of hdcg_spmv_slab: ranges start and end
+                                at multiples of it (or at n_blocks); >1 when tiles hold several
+                                blocks, lcm(1024, bl) / bl for packed small blocks */
     int64_t device_bytes;
     int64_t max_seg_per_block; /* most segments in one block (selects the SpMV kernel) */
+    int64_t packed_stages; /* >0: small blocks also stored tile-packed (1024-value stages) */
 } hdcg_info;
 
 /* ---- runtime ------------------------------------------------------------ */

@@ -21,8 +21,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libhdcgpu.so")
-SOURCES = ["spmv.cu", "spmv_tma.cu", "convert.cu", "analyze.cu", "host_spmv.cu", "membench.cu", "mmio.cu",
-           "capi.cu"]
+SOURCES = ["spmv.cu", "spmv_tma.cu", "convert.cu", "pack.cu", "analyze.cu", "host_spmv.cu", "membench.cu",
+           "mmio.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
@@ -42,18 +42,23 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_lib(verbose=False, force=False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build_lib(verbose=False, force=False, variant="", defines=()) -> str:
+    """The library; `variant` builds an A/B copy (libhdcgpu_<variant>.so, loaded
+    with HDCG_LIBRARY) with extra -D `defines`, in its own object directory."""
+    obj_dir = BUILD + (f"_{variant}" if variant else "")
+    lib = LIB if not variant else os.path.join(PKG, f"libhdcgpu_{variant}.so")
+    extra = [f"-D{d}" for d in defines]
+    os.makedirs(obj_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "hdcgpu.h"))
     objs = []
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(obj_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC] + _flags() + ["-c", s, "-o", o])
+            jobs.append([NVCC] + _flags() + extra + ["-c", s, "-o", o])
 
     def run(cmd):
         if verbose:
@@ -66,10 +71,10 @@ def build_lib(verbose=False, force=False) -> str:
 
     with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run([NVCC] + ARCH + ["-shared", "-ccbin", HOST_CXX, "-o", LIB] + objs +
+    if force or jobs or _stale(lib, objs):
+        run([NVCC] + ARCH + ["-shared", "-ccbin", HOST_CXX, "-o", lib] + objs +
             ["-lcudart_static", "-lrt", "-lpthread", "-ldl"])
-    return LIB
+    return lib
 
 
 def build_oracle(verbose=False):
@@ -90,8 +95,10 @@ def main(argv=None):
     ap.add_argument("--all", action="store_true")
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--variant", default="", help="A/B build: libhdcgpu_<variant>.so")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D for --variant builds")
     a = ap.parse_args(argv)
-    print(build_lib(verbose=a.verbose, force=a.force))
+    print(build_lib(verbose=a.verbose, force=a.force, variant=a.variant, defines=a.defines))
     if a.all:
         build_oracle(verbose=a.verbose)
 

@@ -104,6 +104,7 @@ void stage_csr(Staged& s, int64_t n_rows, int64_t n_cols, int64_t row0, int64_t 
 void account(Matrix* m) {
     m->device_bytes = sizeof(int32_t) * (m->n_blocks + 1 + m->n_seg + m->n_rows + 1 + m->nnz_rest) +
                       sizeof(double) * (m->n_seg * m->bl + m->nnz_rest);
+    if (m->packed) m->device_bytes += sizeof(double) * m->pk_stages * PACK_TILE;  // + small tables
 }
 
 template <class T>
@@ -177,6 +178,9 @@ void matrix_release(Matrix* m) {
     cudaFree(m->rest_rp);
     cudaFree(m->rest_col);
     cudaFree(m->rest_val);
+    cudaFree(m->pk_val);
+    cudaFree(m->pk_meta);
+    cudaFree(m->pk_tab);
     for (PipeCtx* c : m->pipe_all) pipe_ctx_release(c);
     cudaSetDevice(prev);
     delete m;
@@ -369,6 +373,7 @@ hdcg_status hdcg_upload_mhdc(int64_t n, int64_t bl, const int32_t* dia_ptr, int6
             m->dia_slots = slots;
             m->nnz_input = dia_nnz + nnz_rest;
             HDCG_CUDA(cudaStreamSynchronize(st));
+            build_packed(m, st);
         } catch (...) {
             matrix_release(m);
             throw;
@@ -477,9 +482,11 @@ hdcg_status hdcg_get_info(hdcg_matrix h, hdcg_info* info) {
         info->nnz_input = m->nnz_input;
         info->n_tiles = t.n_tiles;
         info->tile_rows = t.tile_rows;
-        info->blocks_per_tile = t.blocks_per_tile > 0 ? t.blocks_per_tile : 1;
+        // the block-range granularity of hdcg_spmv_slab (whole tiles)
+        info->blocks_per_tile = t.align_blocks;
         info->device_bytes = m->device_bytes;
         info->max_seg_per_block = m->max_seg_per_block;
+        info->packed_stages = m->packed ? m->pk_stages : 0;
     });
 }
 

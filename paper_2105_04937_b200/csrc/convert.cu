@@ -688,6 +688,7 @@ void build_mhdc(const CsrInput& in, double theta, int64_t bl, Matrix* m, cudaStr
         Selection s = select_blocked<int32_t>(in, theta, bl, nb, st);
         finish_build<int32_t>(in, bl, nb, s, m, st);
     }
+    build_packed(m, st);  // small blocks: the tile-packed copy the SpMV streams
 }
 
 void build_hdc(const CsrInput& in, double theta, Matrix* m, cudaStream_t st) {

@@ -91,6 +91,17 @@ struct Matrix {
     int32_t* rest_rp = nullptr;
     int32_t* rest_col = nullptr;
     double* rest_val = nullptr;
+    // Tile-packed copy of the segments for small blocks (pack.cu; bl < 1024 where
+    // 1024-row tiles do not hold whole blocks): tile t = rows [1024 t, 1024 t +
+    // 1024) is K_t stages of 1024 values, stage k holding the k-th segment of each
+    // row's block (0.0 where that block has fewer), so the SpMV streams whole
+    // 8 KB stages with 4 rows per thread whatever bl is.  The reference layout
+    // above stays the source of truth (export, rates, the general kernel).
+    bool packed = false;
+    double* pk_val = nullptr;     // stages * 1024 doubles
+    int4* pk_meta = nullptr;      // per tile {first stage, K_t | uniform << 16, table start, first block}
+    int32_t* pk_tab = nullptr;    // per tile: [blocks of the tile][K_t] offsets (one list when uniform)
+    int64_t pk_stages = 0;
     // lazily built state of the host-buffer SpMV pipeline (host_spmv.cu): the
     // chunk plan is shared; each concurrent caller borrows its own context
     // (device x/y buffers, streams, events), so calls on disjoint outputs run
@@ -123,16 +134,24 @@ struct Tiling {
     int rows_per_thread;   // 2 (double2 segment loads) or 1 (odd bl)
     int64_t tile_rows;     // threads * rows_per_thread
     int64_t tiles_per_block;  // > 0 when bl >= tile_rows
-    int64_t blocks_per_tile;  // > 0 when bl <  tile_rows
+    int64_t blocks_per_tile;  // > 0 when bl <  tile_rows and tiles hold whole blocks
     int64_t n_tiles;
+    bool packed = false;      // tile-packed small blocks: tile t = rows [t*tile_rows, ...)
+    int64_t align_blocks = 1; // block ranges must start/end at multiples of this (or at n)
 };
 Tiling tiling_of(const Matrix& m);
+constexpr int64_t PACK_TILE = 1024;  // rows per tile of the packed layout
+bool pack_eligible(int64_t bl, int64_t n_rows);
 
 // Rows [lo, hi) of tile t (lo >= hi for the empty tail tiles of a short last block).
+// tiles_per_block == blocks_per_tile == 0: packed tiles of tile_rows_n rows.
 __host__ __device__ inline void tile_rows(int64_t t, int64_t tiles_per_block, int64_t blocks_per_tile,
                                           int64_t tile_rows_n, int64_t bl, int64_t n_rows, int64_t* lo,
                                           int64_t* hi) {
-    if (tiles_per_block > 0) {
+    if (tiles_per_block == 0 && blocks_per_tile == 0) {
+        *lo = t * tile_rows_n;
+        *hi = *lo + tile_rows_n < n_rows ? *lo + tile_rows_n : n_rows;
+    } else if (tiles_per_block > 0) {
         const int64_t b = t / tiles_per_block;
         const int64_t b0 = b * bl;
         const int64_t bend = b0 + bl < n_rows ? b0 + bl : n_rows;
@@ -194,6 +213,8 @@ void build_csr(const CsrInput& in, Matrix* out, cudaStream_t st);
 int64_t census(const CsrInput& in, int64_t bl, int64_t* block_ptr_host, int32_t* offsets_host,
                int64_t* counts_host, cudaStream_t st);
 void rates(const Matrix& m, double* alpha, double* beta, int64_t* slots, cudaStream_t st);
+// the tile-packed copy of a finished M-HDC (pack.cu); no-op unless pack_eligible
+void build_packed(Matrix* m, cudaStream_t st);
 // (theta, bl) sweep from one census per block width (analyze.cu)
 void analyze(const CsrInput& in, const double* thetas, int n_theta, const int64_t* bls, int n_bl, double* out,
              cudaStream_t st);

@@ -28,6 +28,7 @@
 //     order (bitwise order preserved, no warp-tree reordering);
 //   * y is written once (streaming store); optional fused epilogue emits the
 //     tile's sum of y_i^2 (power iteration) in a fixed reduction order.
+#include <algorithm>
 #include <cstdlib>
 
 #include "hdcg_internal.cuh"
@@ -65,14 +66,20 @@ struct SpmvArgs {
 // IL: interleaved rows (thread t owns tile rows t, t+256, ...) -- tiles inside
 // one block, the TMA kernel's mapping (so per-tile sums agree bitwise); otherwise
 // (whole blocks per tile) R consecutive rows per thread.
-template <int R, bool SCALE, bool NORM, bool IL>
+// PK: the packed tiling (tile = tile_rows consecutive rows, interleaved over the
+// threads, rows of one thread possibly in different blocks) -- the bitwise
+// cross-check of the packed TMA kernel; reads the reference layout.
+template <int R, bool SCALE, bool NORM, bool IL, bool PK = false>
 __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
     __shared__ double prod[REST_CHUNK];
     __shared__ double warp_sums[SPMV_THREADS / 32];
 
     const int64_t tile = a.tile_begin + blockIdx.x;
     int64_t lo, hi;
-    if (a.tiles_per_block > 0) {
+    if (PK) {
+        lo = tile * a.tile_rows;
+        hi = min(lo + a.tile_rows, a.n_rows);
+    } else if (a.tiles_per_block > 0) {
         const int64_t b = tile / a.tiles_per_block;
         const int64_t t = tile - b * a.tiles_per_block;
         const int64_t b0 = b * a.bl;
@@ -87,13 +94,13 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
     // bl = 256 multi-block tiles without a remainder: the TMA kernel's mapping --
     // lane l of block k's two warps owns block rows 32 (warp & 1) + l + 64 r (per-tile
     // sums then agree bitwise between the kernels)
-    const bool MBIL = !IL && R == 4 && (a.bl == 256 || a.bl == 128) && !a.has_rest;
+    const bool MBIL = !PK && !IL && R == 4 && (a.bl == 256 || a.bl == 128) && !a.has_rest;
     const int wpb = MBIL ? (int)a.bl / 128 : 1;
     const int warp = threadIdx.x >> 5, qb = warp / wpb;
     const int64_t mb0 = (int64_t)qb * a.bl + (warp - qb * wpb) * 32 + (threadIdx.x & 31);
     auto row = [&](int r) -> int64_t {
         if (MBIL) return lo + mb0 + (int64_t)32 * wpb * r;
-        return IL ? lo + threadIdx.x + (int64_t)SPMV_THREADS * r : lo + (int64_t)R * threadIdx.x + r;
+        return IL || PK ? lo + threadIdx.x + (int64_t)SPMV_THREADS * r : lo + (int64_t)R * threadIdx.x + r;
     };
 
     double acc[R];
@@ -138,7 +145,27 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 
     // ---- diagonal segments of this row's block, stored order ----------------
     const int64_t i0 = row(0);
-    if (i0 < hi) {
+    if (PK) {  // each row with its own block's segments
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = row(r);
+            if (i >= hi) continue;
+            const int64_t b = i / a.bl, l = i - b * a.bl;
+            const int k0 = __ldg(a.dia_ptr + b), k1 = __ldg(a.dia_ptr + b + 1);
+            for (int k = k0; k < k1; ++k) {
+                const int64_t o = __ldg(a.dia_off + k);
+                const int64_t j = a.row0 + i + o;
+                const double v = __ldcs(a.seg + (int64_t)k * a.bl + l);
+                double xx = (j >= 0 && j < a.n_cols) ? __ldg(a.x + (i + o)) : 0.0;
+                if (SCALE) xx = __dmul_rn(xx, sc);
+                acc[r] = __dadd_rn(acc[r], __dmul_rn(v, xx));
+            }
+            __stcs(a.y + i, acc[r]);
+            if (a.peer_lo && i < a.halo) a.peer_lo[i] = acc[r];
+            if (a.peer_hi && i >= a.n_rows - a.halo) a.peer_hi[i - (a.n_rows - a.halo)] = acc[r];
+        }
+        if (a.peer_lo || a.peer_hi) __threadfence_system();
+    } else if (i0 < hi) {
         const int64_t b = i0 / a.bl;  // all of this thread's rows are in one block
         const int64_t l = i0 - b * a.bl;
         const int k0 = __ldg(a.dia_ptr + b);
@@ -244,6 +271,17 @@ __global__ void __launch_bounds__(SPMV_THREADS) spmv_kernel(const SpmvArgs a) {
 Tiling tiling_of(const Matrix& m) {
     Tiling t;
     const int64_t t4 = 4 * SPMV_THREADS;
+    if (m.packed) {  // tile-packed small blocks (pack.cu): 1024-row tiles, 4 rows per thread
+        t.rows_per_thread = 4;
+        t.tile_rows = PACK_TILE;
+        t.tiles_per_block = t.blocks_per_tile = 0;
+        t.n_tiles = ceil_div(m.n_rows, PACK_TILE);
+        t.packed = true;
+        int64_t a = PACK_TILE, b = m.bl;  // block ranges align to lcm(1024, bl) rows
+        while (b) { const int64_t r = a % b; a = b; b = r; }
+        t.align_blocks = PACK_TILE / a;
+        return t;
+    }
     // 4 rows/thread up to 32 segments per block: with the interleaved row mapping
     // config 2 (27 segments) went 90% -> 97% of peak (profiles/r01_v18_r4_c2_ab.log)
     static const int r4_max_seg = getenv("HDCG_R4_MAXSEG") ? atoi(getenv("HDCG_R4_MAXSEG")) : 32;  // A/B knob
@@ -261,11 +299,18 @@ Tiling tiling_of(const Matrix& m) {
         t.blocks_per_tile = t.tile_rows / m.bl;
         t.n_tiles = ceil_div(m.n_blocks, t.blocks_per_tile);
     }
+    t.align_blocks = t.blocks_per_tile > 0 ? t.blocks_per_tile : 1;
     return t;
 }
 
 template <int R, bool SCALE, bool NORM>
 static void launch_t(const SpmvArgs& a, int64_t n_tiles, cudaStream_t st) {
+    if constexpr (R == 4) {
+        if (a.tiles_per_block == 0 && a.blocks_per_tile == 0) {
+            spmv_kernel<4, SCALE, NORM, false, true><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
+            return;
+        }
+    }
     if (a.tiles_per_block > 0) spmv_kernel<R, SCALE, NORM, true><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
     else spmv_kernel<R, SCALE, NORM, false><<<(unsigned)n_tiles, SPMV_THREADS, 0, st>>>(a);
 }
@@ -288,7 +333,14 @@ void spmv_launch(const Matrix& m, const double* x_local, double* y, int64_t bloc
         fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: block range outside the matrix");
     const Tiling t = tiling_of(m);
     int64_t tile_begin, tile_end;
-    if (t.tiles_per_block > 0) {
+    if (t.packed) {
+        auto aligned = [&](int64_t b) { return b % t.align_blocks == 0 || b * m.bl >= m.n_rows; };
+        if (!aligned(block_begin) || !aligned(block_end))
+            fail(HDCG_ERR_INVALID_ARGUMENT, "spmv: block range not aligned to the packed 1024-row tiles");
+        tile_begin = std::min(block_begin * m.bl, m.n_rows) / PACK_TILE;
+        tile_end = ceil_div(std::min(block_end * m.bl, m.n_rows), PACK_TILE);
+        if (block_begin == block_end) tile_end = tile_begin;
+    } else if (t.tiles_per_block > 0) {
         tile_begin = block_begin * t.tiles_per_block;
         tile_end = block_end * t.tiles_per_block;
     } else {

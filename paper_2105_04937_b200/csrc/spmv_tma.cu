@@ -51,11 +51,17 @@ constexpr int XGROUP_ROWS = 16;          // x values loaded ahead per thread (se
 constexpr int WPASS = 256;               // remainder scratch per warp (entries per pass <= this)
 // fused remainder mode (REST == 3): gather warps sum the CSR remainder of the
 // tiles ahead into shared memory while the consumers stream segments
-constexpr int GATHER_WARPS = 4;
+#ifndef HDCG_GATHER_WARPS
+#define HDCG_GATHER_WARPS 16
+#endif
+constexpr int GATHER_WARPS = HDCG_GATHER_WARPS;  // with 8 consumers + the producer: one CTA per SM
 constexpr int GPER = 8;                  // x gathers per lane per pass
 constexpr int GPASS = 32 * GPER;         // entries per gather-warp pass
 constexpr int RS_BUFS = 3;               // tiles of remainder sums in flight
-__host__ __device__ constexpr int gather_rows_per_warp(int R) { return 256 * R / GATHER_WARPS; }
+// rows per gather warp: whole 32-row runs (R = 1: only 8 of the gather warps have rows)
+__host__ __device__ constexpr int gather_rows_per_warp(int R) {
+    return 32 * ((8 * R + GATHER_WARPS - 1) / GATHER_WARPS);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -131,6 +137,9 @@ struct TmaArgs {
     int64_t halo;
     int prefetch;  // producer prefetches the consumers' tile-start lines into L2
     int fused;     // REST == 3: remainder sums by the gather warps (shared memory)
+    const double* pk_val;  // LAY 5: the tile-packed segment copy (pack.cu)
+    const int4* pk_meta;
+    const int32_t* pk_tab;
 };
 
 struct Geo {
@@ -138,9 +147,16 @@ struct Geo {
     int b;
 };
 
-template <int R, bool MB>
+template <int R, bool MB, bool PK = false>
 __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
     Geo g;
+    if constexpr (PK) {  // packed: 1024 consecutive rows, b = the tile's first block
+        g.lo = (int64_t)tile * (CONSUMERS * R);
+        g.hi = min(g.lo + (int64_t)(CONSUMERS * R), a.n_rows);
+        g.b = (int)(g.lo / a.bl);
+        g.b0 = (int64_t)g.b * a.bl;
+        return g;
+    }
     if constexpr (MB) {  // G whole blocks: b = the first one
         g.b = tile * a.blocks_per_tile;
         g.b0 = g.lo = (int64_t)g.b * a.bl;
@@ -446,12 +462,14 @@ __device__ __forceinline__ void gather_rest_rows(const TmaArgs& a, int64_t w0, i
 // bl = 256 / 128 without a remainder, rows interleaved inside each block.
 // REST == 3 (fused): warps 9 .. 9+GATHER_WARPS-1 are gather warps (remainder
 // sums of the tiles ahead into shared memory, RS_BUFS tiles in flight); the
-// consumers start each row from its sum.  Two CTAs per SM.
+// consumers start each row from its sum.  One CTA per SM: the x gathers need
+// about as many warps in flight as rest_pipe_kernel has (24 per SM).
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
-__global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS, REST == 3 ? 2 : 3)
+__global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS, REST == 3 ? 1 : 3)
     spmv_tma_kernel(const TmaArgs a) {
     constexpr bool MB = LAY == 1 || LAY == 3 || LAY == 4;
     constexpr bool ODD = LAY == 2;
+    constexpr bool PK = LAY == 5;  // tile-packed small blocks (pack.cu), R = 4
     constexpr int TILE = CONSUMERS * R;
     constexpr int STRIDE = ring_stride(R);
     // x registers per thread stay at XGROUP_ROWS doubles (8 for the multi-block layout
@@ -490,7 +508,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
             uint32_t rph = 0;
             bool wrapped = false;
             for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-                const Geo g = geo<R, MB>(a, tile);
+                const Geo g = geo<R, MB, PK>(a, tile);
                 if (g.lo >= g.hi) continue;  // the consumers skip it too
                 if (wrapped) mbar_wait(&S.rs_empty[rb], rph ^ 1u);
                 const int64_t w0 = g.lo + (int64_t)gw * GROWS;
@@ -520,7 +538,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         uint32_t pphase = 0;     // parity of that stage's current use
         bool p_wrapped = false;  // every stage has been used once
         for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-            const Geo g = geo<R, MB>(a, tile);
+            const Geo g = geo<R, MB, PK>(a, tile);
             if (g.lo >= g.hi) continue;
             if (a.prefetch && lane == 0) {
                 if constexpr (REST == 1) {
@@ -550,6 +568,22 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
                     }
                     __syncwarp();
                     if (j < cnt) bulk_g2s(S.ring + ps * STRIDE + lane * a.bl, src, pb, &S.full[ps], policy);
+                    if (++ps == NS) {
+                        ps = 0;
+                        pphase ^= 1u;
+                        p_wrapped = true;
+                    }
+                }
+                continue;
+            }
+            if constexpr (PK) {  // K_t whole 8 KB stages, contiguous
+                const int4 md = __ldg(a.pk_meta + tile);
+                const int K = md.y & 0xffff;
+                const double* src = a.pk_val + (int64_t)md.x * TILE;
+                for (int k = 0; k < K; ++k, src += TILE) {
+                    if (p_wrapped) mbar_wait(&S.empty[ps], pphase ^ 1u);
+                    mbar_expect_tx(&S.full[ps], TILE * 8u);
+                    bulk_g2s(S.ring + ps * STRIDE, src, TILE * 8u, &S.full[ps], policy);
                     if (++ps == NS) {
                         ps = 0;
                         pphase ^= 1u;
@@ -612,7 +646,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
     int rb = 0;          // REST == 3: remainder-sum buffer of this tile
     uint32_t rph = 0;
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
-        const Geo g = geo<R, MB>(a, tile);
+        const Geo g = geo<R, MB, PK>(a, tile);
         if (g.lo >= g.hi) {
             if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
             continue;
@@ -663,7 +697,16 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         // [k0, kw): this warp's block's segments (MB: k1 - k0 is the largest
         // segment count over the tile's blocks; otherwise kw = k1, the one block's).
         int k0, k1, kw;
-        if constexpr (MB) {  // warp-uniform: bl % (32 R) == 0
+        const int32_t* offs = a.dia_off;  // the offsets [k0, k1) index
+        bool uniform = true;              // PK: every block of the tile has the same offsets
+        int4 md = make_int4(0, 0, 0, 0);
+        if constexpr (PK) {
+            md = __ldg(a.pk_meta + tile);
+            k0 = 0;
+            k1 = kw = md.y & 0xffff;
+            uniform = (md.y >> 16) & 1;
+            offs = a.pk_tab + md.z;
+        } else if constexpr (MB) {  // warp-uniform: bl % (32 R) == 0
             const int64_t bw = (int64_t)g.b + (mbil ? qb : t0 / (int)a.bl);
             const int nbt = (int)min((int64_t)a.blocks_per_tile, a.n_blocks - g.b);
             k0 = bw < a.n_blocks ? __ldg(a.dia_ptr + bw) : 0;
@@ -676,11 +719,63 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         }
         const double* xrow = a.x + g.lo;
         const bool full = rows == TILE;  // warp-uniform: no per-row predicates needed
+        if (PK && !uniform) {
+            // packed tile whose blocks differ: each row looks its k-th offset up in
+            // its block's list (INT32_MIN: that block has no k-th segment -- skip)
+            int q[R];
+            const int rel = (int)(g.lo - (int64_t)md.w * a.bl);  // < bl
+#pragma unroll
+            for (int r = 0; r < R; ++r) q[r] = (rel + lr(r)) / (int)a.bl * k1;
+            constexpr int XGN = XG / 2 > 0 ? XG / 2 : 1;  // per-row offsets: fewer x registers
+            for (int kg = 0; kg < k1; kg += XGN) {
+                const int ng = min(XGN, k1 - kg);
+                double xv[XGN][R];
+                uint32_t okm = 0;  // bit u*R + r: row r has a k-th segment
+#pragma unroll
+                for (int u = 0; u < XGN; ++u)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        xv[u][r] = 0.0;
+                        if (u < ng && lr(r) < rows) {
+                            const int o = __ldg(offs + q[r] + kg + u);
+                            const int64_t j = g.lo + lr(r) + (int64_t)o;
+                            if (o != INT32_MIN) {
+                                okm |= 1u << (u * R + r);
+                                if (j >= xlo_valid && j < xhi_valid) xv[u][r] = __ldg(xrow + lr(r) + o);
+                            }
+                        }
+                    }
+#pragma unroll
+                for (int u = 0; u < XGN; ++u) {
+                    if (u < ng) {
+                        mbar_wait(&S.full[cs], cphase);
+                        const double* st = S.ring + cs * STRIDE;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const double v = st[lr(r)];
+                            double xx = xv[u][r];
+                            if (SCALE) xx = __dmul_rn(xx, sc);
+                            if ((okm >> (u * R + r)) & 1u) acc[r] = __dadd_rn(acc[r], __dmul_rn(v, xx));
+                            else asm volatile("" ::"d"(v));
+                        }
+#pragma unroll
+                        for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&S.empty[cs]);
+                        if (++cs == NS) {
+                            cs = 0;
+                            cphase ^= 1u;
+                        }
+                    }
+                }
+            }
+            k1 = k0;  // done: skip the uniform loop below
+        }
         for (int kb0 = k0; kb0 < k1; kb0 += 32) {
             // the next <= 32 offsets of the block: one coalesced load, then shuffles
             const int nk = min(32, k1 - kb0);
             const int nko = MB ? min(32, kw - kb0) : nk;  // of which this warp's block has
-            const int my_off = lane < nko ? __ldg(a.dia_off + kb0 + lane) : 0;
+            const int my_off = lane < nko ? __ldg(offs + kb0 + lane) : 0;
             for (int kg = 0; kg < nk; kg += XG) {
                 const int ng = min(XG, nk - kg);  // warp-uniform
                 const int nv = MB ? min(ng, kw - kb0 - kg) : ng;  // of which this warp's block has
@@ -1089,6 +1184,7 @@ void launch_m(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cu
 template <int R>
 void launch_r(const TmaArgs& a, int grid, size_t smem, bool scale, bool norm, cudaStream_t st) {
     if constexpr (R == 4) {
+        if (a.pk_meta) return launch_m<4, 5>(a, grid, smem, scale, norm, st);
         if (a.blocks_per_tile > 0) {
             // bl = 256 without a remainder: block-local interleaved rows (tile layout 3)
             const bool plain = !a.has_rest && !a.init_y && !a.fused;
@@ -1126,7 +1222,8 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     const char* eb = getenv("HDCG_BLK");
     const bool blk = (!eb || atoi(eb) != 0) && t.blocks_per_tile > 0 && R == 1 && m.bl >= CONSUMERS / BLK_MAX_G &&
                      m.bl < CONSUMERS && m.max_seg_per_block <= BLK_MAX_SEG;
-    if (!blk && t.tiles_per_block <= 0 && (R != 4 || t.blocks_per_tile <= 0 || m.bl % (32 * R) != 0)) return false;
+    if (!blk && !t.packed && t.tiles_per_block <= 0 && (R != 4 || t.blocks_per_tile <= 0 || m.bl % (32 * R) != 0))
+        return false;
     if (tile_end <= tile_begin) return true;
     TmaArgs a;
     a.dia_ptr = m.dia_ptr;
@@ -1150,6 +1247,9 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     a.tile_end = (int)tile_end;
     a.has_rest = m.nnz_rest > 0;
     a.init_y = 0;
+    a.pk_val = t.packed ? m.pk_val : nullptr;
+    a.pk_meta = t.packed ? m.pk_meta : nullptr;
+    a.pk_tab = t.packed ? m.pk_tab : nullptr;
     a.y_vec_ok = ((uintptr_t)y % 16) == 0;  // (odd bl: tiles may start on odd rows, tested per thread)
     a.peer_lo = peer.lo;
     a.peer_hi = peer.hi;
@@ -1248,7 +1348,7 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
             HDCG_LAUNCH_CHECK("spmv_blk_kernel");
             return;
         }
-        if (b.fused) want_ctas = std::min(want_ctas, 2);  // 13 warps per CTA: 2 per SM
+        if (b.fused) want_ctas = 1;  // 25 warps per CTA: one per SM
         const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
         const size_t fixed = smem_bytes(R, 0, b.has_rest, b.fused);
         const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;

@@ -81,7 +81,7 @@ class Info(C.Structure):
                 ("n_blocks", C.c_int64), ("n_seg", C.c_int64), ("nnz_rest", C.c_int64),
                 ("dia_slots", C.c_int64), ("nnz_input", C.c_int64), ("n_tiles", C.c_int64),
                 ("tile_rows", C.c_int64), ("blocks_per_tile", C.c_int64),
-                ("device_bytes", C.c_int64), ("max_seg_per_block", C.c_int64)]
+                ("device_bytes", C.c_int64), ("max_seg_per_block", C.c_int64), ("packed_stages", C.c_int64)]
 
 
 _lib = None
@@ -557,6 +557,9 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     (mirrors spmv.cu::tiling_of and spmv_tma.cu::spmv_tma_launch)."""
     r = info.tile_rows // 256
     b = lambda v: str(v).lower()  # noqa: E731
+    if info.packed_stages > 0:  # tile-packed small blocks (pack.cu)
+        rest = 0 if info.nnz_rest == 0 else (3 if info.nnz_rest * 4 >= info.n_rows else 1)
+        return [f"hdcg::spmv_tma_kernel<4,{b(scale)},{b(norm)},{rest},5>"]
     inside = info.bl >= info.tile_rows  # tiles inside one block, else whole blocks per tile
     mb = not inside and r == 4 and info.bl % 128 == 0
     blk = not inside and r == 1 and 8 <= info.bl < 256 and info.max_seg_per_block <= 16

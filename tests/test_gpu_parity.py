@@ -536,12 +536,15 @@ def test_kernel_paths_bitwise_identical(port, shape):
         H.set_kernel_policy(H.POLICY_AUTO)
 
 
+@pytest.mark.parametrize("packed", ["1", "0"])
 @pytest.mark.parametrize("bl", [96, 100, 150, 200])
-def test_blk_tiles_per_stage_block_ranges(port, bl):
-    """spmv_blk_kernel (8 <= bl < 256, whole blocks per tile) over tile-aligned block
-    ranges that split the persistent grid's schedule: y equals the oracle bit for bit,
-    with and without x_scale, with a light remainder (in the kernel) and a heavy one
-    (rest kernel first, init_y)."""
+def test_blk_tiles_per_stage_block_ranges(port, bl, packed, monkeypatch):
+    """Small blocks over tile-aligned block ranges that split the persistent grid's
+    schedule -- the tile-packed layout (default; 1024-row tiles, ranges aligned to
+    lcm(1024, bl) rows) and spmv_blk_kernel (HDCG_PACKED=0; whole blocks per
+    256-row tile): y equals the oracle bit for bit, with and without x_scale, with a
+    light remainder (in the kernel) and a heavy one (gather warps / summed first)."""
+    monkeypatch.setenv("HDCG_PACKED", packed)
     rng = np.random.default_rng(23)
     rp, col, val = synth.laplacian7(36, 30, 28)
     n = len(rp) - 1
@@ -557,9 +560,13 @@ def test_blk_tiles_per_stage_block_ranges(port, bl):
         want_sc = port.spmv_mhdc(ref, x * 0.5)
         assert H.spmv_mhdc(m, x).tobytes() == want.tobytes(), bl
         nb = m.n_blocks
+        assert (m.info.packed_stages > 0) == (packed == "1"), bl
         sc = torch.tensor([0.5], dtype=torch.float64, device="cuda")
-        G = 256 // bl  # blocks per tile: block ranges are tile-aligned
+        G = m.info.blocks_per_tile  # block ranges are tile-aligned
+        if packed == "0":
+            assert G == 256 // bl
         for cuts in ((0, 3 * G, nb), (0, 7 * G, 8 * G, 29 * G, G * ((nb - 1) // G), nb), (0, G * (nb // (3 * G)), nb)):
+            cuts = sorted(set(min(c, nb) for c in cuts))
             y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
             ys = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
             for b0, b1 in zip(cuts[:-1], cuts[1:]):
@@ -571,10 +578,13 @@ def test_blk_tiles_per_stage_block_ranges(port, bl):
         m.free()
 
 
-def test_blk_several_tiles_per_cta(port):
-    """spmv_blk_kernel with several tiles per persistent CTA (64^3 rows, bl = 100 / 50 /
-    10, so the stage ring wraps): the oracle's y bit for bit, with x_scale and the fused
-    per-tile norm, with a light remainder (in the kernel) and a heavy one (summed first)."""
+@pytest.mark.parametrize("packed", ["1", "0"])
+def test_blk_several_tiles_per_cta(port, packed, monkeypatch):
+    """Small blocks with several tiles per persistent CTA (64^3 rows, bl = 100 / 50 /
+    10, so the stage ring wraps), tile-packed (default) and spmv_blk_kernel
+    (HDCG_PACKED=0): the oracle's y bit for bit, with x_scale and the fused per-tile
+    norm, with a light remainder (in the kernel) and a heavy one."""
+    monkeypatch.setenv("HDCG_PACKED", packed)
     rng = np.random.default_rng(31)
     rp, col, val = synth.laplacian7(64, 64, 64)
     n = len(rp) - 1
@@ -587,7 +597,8 @@ def test_blk_several_tiles_per_cta(port):
         for bl in (100, 50, 10):
             ref = port.to_mhdc(rp2, col2, val2, 0.6, bl)
             m = H.to_mhdc(csr(rp2, col2, val2), 0.6, bl)
-            assert any("blk" in k for k in H.spmv_kernels(m.info)), bl
+            want_k = "blk" if packed == "0" else ",5>"
+            assert any(want_k in k for k in H.spmv_kernels(m.info)), (bl, H.spmv_kernels(m.info))
             assert H.spmv_mhdc(m, x).tobytes() == port.spmv_mhdc(ref, x).tobytes(), bl
             y = torch.empty(n, dtype=torch.float64, device="cuda")
             tiles = torch.empty(m.info.n_tiles, dtype=torch.float64, device="cuda")
