@@ -58,7 +58,12 @@ void call(hdcg_status s) {
     if (s != HDCG_OK) rethrow(s);
 }
 
-// index_t is int32 in the default build; an HDC_INDEX64 build narrows here.
+// index_t is int32 in the default build.  An HDC_INDEX64 build (types.hpp:8-12)
+// passes input row pointers through as int64 (RowPtrArg) and narrows the other
+// index arrays here: the device formats index rows, columns, segments and
+// remainder entries with int32 (n, n_seg, nnz_rest < 2^31; the segment values
+// themselves are addressed with 64-bit arithmetic), and a value beyond that range
+// raises std::overflow_error like the reference's own range checks.
 struct I32View {
     std::vector<int32_t> tmp;
     const int32_t* ptr = nullptr;
@@ -75,6 +80,16 @@ struct I32View {
             ptr = tmp.data();
         }
     }
+};
+
+// An input CSR's row pointer: passed through as is -- int32 in the default build,
+// int64 with HDCG_ROWPTR_I64 in an HDC_INDEX64 build (nnz may then exceed 2^31,
+// e.g. BASELINE config 4's 3.75e9 entries).  Column indices stay < n < 2^31.
+struct RowPtrArg {
+    const void* ptr;
+    unsigned flags;
+    explicit RowPtrArg(std::span<const index_t> s)
+        : ptr(s.data()), flags(sizeof(index_t) == sizeof(int64_t) ? HDCG_ROWPTR_I64 : 0u) {}
 };
 
 template <class T>
@@ -266,10 +281,11 @@ Ident ident(const MHdcMatrix& m) {
 hdcg_matrix device_of(const CsrMatrix& m) {
     const Ident id = ident(m);
     if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
-    const I32View rp(m.row_ptr()), col(m.col_ind());
+    const RowPtrArg rp(m.row_ptr());
+    const I32View col(m.col_ind());
     hdcg_matrix h = nullptr;
-    call(hdcg_build_csr(m.n(), static_cast<int64_t>(m.values().size()), rp.ptr, col.ptr, m.values().data(), 0,
-                        nullptr, &h));
+    call(hdcg_build_csr(m.n(), static_cast<int64_t>(m.values().size()), rp.ptr, col.ptr, m.values().data(),
+                        rp.flags, nullptr, &h));
     cache().put(id.key, id.hash, h);
     return h;
 }
@@ -340,7 +356,8 @@ Exported export_all(hdcg_matrix h) {
 // Input CSR handed to the device converters.  The reference's CsrMatrix is
 // already validated by its constructor, so no HDCG_VALIDATE here.
 struct CsrArgs {
-    I32View rp, col;
+    RowPtrArg rp;
+    I32View col;
     const CsrMatrix& m;
     explicit CsrArgs(const CsrMatrix& mm) : rp(mm.row_ptr()), col(mm.col_ind()), m(mm) {}
 };
@@ -388,15 +405,16 @@ static DiagonalCensus census_impl(const CsrMatrix& m, index_t bl, bool global) {
     c.bl = global ? m.n() : bl;
     c.n_blocks = m.n() == 0 ? 0 : (m.n() + c.bl - 1) / c.bl;
     c.per_block.resize(static_cast<std::size_t>(c.n_blocks));
-    const I32View rp(m.row_ptr()), col(m.col_ind());
+    const RowPtrArg rp(m.row_ptr());
+    const I32View col(m.col_ind());
     std::vector<int64_t> bp(static_cast<std::size_t>(c.n_blocks) + 1);
     int64_t total = 0;
     const int64_t arg_bl = global ? 0 : bl;
     const int64_t nnz = static_cast<int64_t>(m.values().size());
-    call(hdcg_census(m.n(), nnz, rp.ptr, col.ptr, arg_bl, 0, bp.data(), nullptr, nullptr, &total));
+    call(hdcg_census(m.n(), nnz, rp.ptr, col.ptr, arg_bl, rp.flags, bp.data(), nullptr, nullptr, &total));
     std::vector<int32_t> offs(static_cast<std::size_t>(total));
     std::vector<int64_t> cnt(static_cast<std::size_t>(total));
-    call(hdcg_census(m.n(), nnz, rp.ptr, col.ptr, arg_bl, 0, bp.data(), offs.data(), cnt.data(), &total));
+    call(hdcg_census(m.n(), nnz, rp.ptr, col.ptr, arg_bl, rp.flags, bp.data(), offs.data(), cnt.data(), &total));
     for (index_t b = 0; b < c.n_blocks; ++b)
         for (int64_t k = bp[b]; k < bp[b + 1]; ++k)
             c.per_block[b].push_back(OffsetCount{static_cast<index_t>(offs[k]), static_cast<index_t>(cnt[k])});
@@ -414,7 +432,7 @@ static hdcg_matrix build_hdc_device(const CsrMatrix& m, real_t theta) {
     const CsrArgs a(m);
     hdcg_matrix h = nullptr;
     call(hdcg_build_hdc(m.n(), static_cast<int64_t>(m.values().size()), a.rp.ptr, a.col.ptr, m.values().data(),
-                        theta, 0, nullptr, &h));
+                        theta, a.rp.flags, nullptr, &h));
     return h;
 }
 
@@ -444,7 +462,7 @@ MHdcMatrix to_mhdc(const CsrMatrix& m, real_t theta, index_t bl) {
     const CsrArgs a(m);
     hdcg_matrix h = nullptr;
     call(hdcg_build_mhdc(m.n(), m.n(), 0, static_cast<int64_t>(m.values().size()), a.rp.ptr, a.col.ptr,
-                         m.values().data(), theta, bl, 0, nullptr, &h));
+                         m.values().data(), theta, bl, a.rp.flags, nullptr, &h));
     Exported e = export_all(h);
     MHdcMatrix out(m.n(), bl, widen(e.dia_ptr), widen(e.offsets), std::move(e.segments),
                    CsrMatrix(m.n(), std::move(e.rest_val), widen(e.rest_col), widen(e.rest_rp)), theta);

@@ -4,7 +4,7 @@ current HDCG_* environment knobs.  Matrices are generated once per box call and
 cached under /tmp.  20 launches after 3 warm-up, 256 MB L2 flush before each;
 prints one JSON line per workload (ms, fraction of the measured HBM peak).
 
-    python scripts/ab.py LABEL c1:100 c1:4096 c1:hdc c1:csr c2:4096 c3:8192 c3:1024 c3:hdc
+    python scripts/ab.py LABEL c1-100 c1-4096 c1-hdc c1-csr c2-4096 c3-8192 c3-1024 c3-hdc
 """
 import json
 import os
@@ -42,7 +42,7 @@ def main():
     st = torch.cuda.current_stream().cuda_stream
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
     for spec in sys.argv[2:]:
-        w, fmt = spec.split(":")
+        w, fmt = spec.replace("-", ":").split(":")  # c3-8192 (gpu.sh steps split on ":")
         rp, col, val, seed = matrix(w)
         n = len(rp) - 1
         A = H.CsrMatrix(n, val, col, rp.astype(np.int32))

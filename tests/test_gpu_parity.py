@@ -640,6 +640,20 @@ def test_reference_acceptance_through_gpu_shim():
     assert "all 8 criteria passed" in r.stdout
 
 
+ACCEPT64 = ACCEPT + "64"
+
+
+@pytest.mark.skipif(not os.path.exists(ACCEPT64), reason="acceptance_gpu64 not built (needs /root/reference)")
+def test_reference_acceptance_index64_build():
+    """The same acceptance program in the reference's 64-bit index build
+    (HDC_INDEX64, types.hpp:8-12): the shim passes int64 row pointers through
+    (HDCG_ROWPTR_I64) and narrows the rest; all 8 criteria pass."""
+    r = subprocess.run([ACCEPT64], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(ACCEPT64))
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all 8 criteria passed" in r.stdout
+
+
 CACHE_TEST = os.path.join(os.path.dirname(ACCEPT), "shim_cache_test")
 
 
@@ -963,3 +977,41 @@ def test_remainder_kernel_variants_and_csr(port, variant, monkeypatch):
             assert float(tiles.sum().item()) == pytest.approx(float(np.dot(want, want)), rel=1e-12)
     finally:
         H.set_kernel_policy(H.POLICY_AUTO)
+
+
+def test_concurrent_host_spmv_calls(port):
+    """Concurrent calls on disjoint outputs are allowed: four host
+    threads call spmv_mhdc / spmv_hdc on the same matrices with different x at once
+    (each call borrows its own pipeline context; ctypes releases the GIL), every y
+    bitwise equal to the oracle's."""
+    import threading
+    rp, col, val = synth.laplacian7(48, 40, 36)
+    n = len(rp) - 1
+    A = csr(rp, col, val)
+    m = H.to_mhdc(A, 0.6, 1024)
+    h = H.to_hdc(A, 0.6)
+    ref_m = port.to_mhdc(rp, col, val, 0.6, 1024)
+    ref_h = port.to_hdc(rp, col, val, 0.6)
+    xs = [synth.x_vector(n, 100 + k) for k in range(4)]
+    want = [(port.spmv_mhdc(ref_m, x), port.spmv_mhdc(ref_h, x)) for x in xs]
+    errors = []
+    barrier = threading.Barrier(4)
+
+    def work(k):
+        try:
+            barrier.wait()
+            for _ in range(20):
+                ym = H.spmv_mhdc(m, xs[k])
+                yh = H.spmv_hdc(h, xs[k])
+                if ym.tobytes() != want[k][0].tobytes() or yh.tobytes() != want[k][1].tobytes():
+                    errors.append(k)
+                    return
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
