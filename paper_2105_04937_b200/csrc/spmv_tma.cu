@@ -645,10 +645,21 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
     int rb = 0;          // REST == 3: remainder-sum buffer of this tile
     uint32_t rph = 0;
+    int pe0 = 0, pe1 = 0;  // REST == 1: the next tile's remainder entry range
+    auto probe = [&](int tl) {
+        pe0 = pe1 = 0;
+        if (REST != 1 || tl >= a.tile_end) return;
+        const Geo q = geo<R, MB, PK>(a, tl);
+        if (q.lo >= q.hi) return;
+        pe0 = __ldg(a.rest_rp + q.lo);
+        pe1 = __ldg(a.rest_rp + q.hi);
+    };
+    probe(a.tile_begin + blockIdx.x);
     for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
         const Geo g = geo<R, MB, PK>(a, tile);
         if (g.lo >= g.hi) {
             if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
+            probe(tile + gridDim.x);
             continue;
         }
         const int rows = (int)(g.hi - g.lo);
@@ -677,19 +688,25 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? a.y[g.lo + lr(r)] : 0.0;
         } else if constexpr (REST == 1) {
-            if constexpr (!MB) {  // the warp's rows are R runs of 32
+            // a light remainder: most tiles have no entries.  The tile's entry range
+            // was loaded one tile ahead, so those tiles issue no dependent load here.
+            const bool any = pe0 < pe1;
+            probe(tile + gridDim.x);
+            if (any) {
+                if constexpr (!MB) {  // the warp's rows are R runs of 32
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const int64_t lo = g.lo + (int64_t)CONSUMERS * r;
-                    if (lo >= g.hi) break;
-                    double a1[1] = {0.0};
-                    warp_rest<1, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo,
-                                        min(lo + CONSUMERS, g.hi), warp, lane, S.scratch + warp * WPASS, a1);
-                    acc[r] = a1[0];
+                    for (int r = 0; r < R; ++r) {
+                        const int64_t lo = g.lo + (int64_t)CONSUMERS * r;
+                        if (lo >= g.hi) break;
+                        double a1[1] = {0.0};
+                        warp_rest<1, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, lo,
+                                            min(lo + CONSUMERS, g.hi), warp, lane, S.scratch + warp * WPASS, a1);
+                        acc[r] = a1[0];
+                    }
+                } else {  // R consecutive rows per lane (mbil needs REST == 0)
+                    warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
+                                        S.scratch + warp * WPASS, acc);
                 }
-            } else {  // R consecutive rows per lane (mbil needs REST == 0)
-                warp_rest<R, SCALE>(a.rest_rp, a.rest_col, a.rest_val, a.x, a.row0, sc, g.lo, g.hi, warp, lane,
-                                    S.scratch + warp * WPASS, acc);
             }
         }
 
