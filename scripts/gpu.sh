@@ -11,8 +11,9 @@
 #   bench:NAME:ARGS            python bench.py ARGS (commas -> spaces) > NAME.json
 #   ref:NAME:ARGS              python bench.py --impl reference ARGS > NAME.json
 #   launches:NAME:ARGS         the bench command plain, then ncu's launch list of it
-#   ncu:NAME:REGEX:SKIP:ARGS   the bench command plain, then ncu --set full of the
-#                              first launch of kernels matching REGEX after SKIP
+#   ncu:NAME:REGEX:SKIP:COUNT:ARGS  the bench command plain, then ncu --set full of
+#                              COUNT launches of kernels matching REGEX after SKIP
+#                              ("+" in REGEX stands for "|", which the shell would pipe)
 #   py:NAME:SCRIPT:ARGS        python SCRIPT ARGS > NAME.log
 #   env:VAR=VALUE / unenv:VAR  set / clear an environment variable for the later steps
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
@@ -22,7 +23,7 @@ mkdir -p "$O"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit,temperature.gpu --format=csv > "$O/smi.csv" 2>&1
 st() { echo "$1=$2" >> "$O/status.txt"; }
 for step in "$@"; do
-  IFS=':' read -r kind a1 a2 a3 a4 <<< "$step"
+  IFS=':' read -r kind a1 a2 a3 a4 a5 <<< "$step"
   case $kind in
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$O/smoke.log" 2>&1; st smoke $? ;;
     tests) if [ -n "$a1" ]; then K=(-k "$a1"); else K=(); fi
@@ -36,10 +37,10 @@ for step in "$@"; do
               timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
                   --log-file "$O/$a1.launches.csv" $CMD > "$O/$a1.ncu.log" 2>&1
               st "launches_$a1" $? ;;
-    ncu) CMD="python bench.py ${a4//,/ }"
+    ncu) CMD="python bench.py ${a5//,/ }"
          timeout 900 $CMD > "$O/$a1.plain.log" 2>&1 && \
-         timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:$a2" -s "$a3" -c 1 \
-             -o "$O/$a1" $CMD > "$O/$a1.ncu.log" 2>&1
+         timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:${a2//+/|}" -s "$a3" \
+             -c "$a4" -o "$O/$a1" $CMD > "$O/$a1.ncu.log" 2>&1
          st "ncu_$a1" $? ;;
     env) export "$a1"; echo "env $a1" >> "$O/status.txt" ;;
     unenv) unset "$a1"; echo "unenv $a1" >> "$O/status.txt" ;;
