@@ -50,18 +50,14 @@ constexpr int THREADS = CONSUMERS + 32;  // + producer warp
 constexpr int XGROUP_ROWS = 16;          // x values loaded ahead per thread (segments x rows)
 constexpr int WPASS = 256;               // remainder scratch per warp (entries per pass <= this)
 // fused remainder mode (REST == 3): gather warps sum the CSR remainder of the
-// tiles ahead into shared memory while the consumers stream segments
+// tiles ahead into y while the consumers stream segments
 #ifndef HDCG_GATHER_WARPS
-#define HDCG_GATHER_WARPS 16
+#define HDCG_GATHER_WARPS 15
 #endif
-constexpr int GATHER_WARPS = HDCG_GATHER_WARPS;  // with 8 consumers + the producer: one CTA per SM
+constexpr int GATHER_WARPS = HDCG_GATHER_WARPS;  // + 8 consumers + the producer = 24 warps: one CTA per SM, 80 registers
 constexpr int GPER = 8;                  // x gathers per lane per pass
 constexpr int GPASS = 32 * GPER;         // entries per gather-warp pass
-constexpr int RS_BUFS = 3;               // tiles of remainder sums in flight
-// rows per gather warp: whole 32-row runs (R = 1: only 8 of the gather warps have rows)
-__host__ __device__ constexpr int gather_rows_per_warp(int R) {
-    return 32 * ((8 * R + GATHER_WARPS - 1) / GATHER_WARPS);
-}
+constexpr int RS_SLOTS = 2 * 32;         // tile hand-off barriers (>= 2 * GATHER_WARPS, power of 2)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -177,17 +173,17 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
 __host__ __device__ constexpr int ring_stride(int R) { return CONSUMERS * R + 2; }
 
 // has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
-// fused: the gather warps' remainder sums (RS_BUFS tiles), scratch and row pointers
+// fused: the gather warps' product scratch and staged row pointers (each gather
+// warp sums whole tiles: TILE + 1 row pointers), the tile hand-off barriers
 __host__ __device__ inline size_t fused_int_bytes(int R) {
-    return ((size_t)GATHER_WARPS * (gather_rows_per_warp(R) + 1) * sizeof(int32_t) + 15) & ~size_t(15);
+    return ((size_t)GATHER_WARPS * (CONSUMERS * R + 1) * sizeof(int32_t) + 15) & ~size_t(15);
 }
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest, int fused = 0) {
     size_t b = sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
                                  2 * CONSUMER_WARPS) +
                sizeof(uint64_t) * (2 * nstage);
     if (fused)
-        b += sizeof(double) * ((size_t)RS_BUFS * CONSUMERS * R + GATHER_WARPS * GPASS) + fused_int_bytes(R) +
-             sizeof(uint64_t) * 2 * RS_BUFS;
+        b += sizeof(double) * ((size_t)GATHER_WARPS * GPASS) + fused_int_bytes(R) + sizeof(uint64_t) * 2 * RS_SLOTS;
     return b;
 }
 
@@ -195,12 +191,11 @@ struct Smem {
     double* ring;     // nstage * ring_stride(R)
     double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
     double* wsum;     // 2 * CONSUMER_WARPS (fused norm: double-buffered warp partials)
-    double* rsum;     // fused: RS_BUFS * TILE remainder sums, tile-local rows
     double* gscratch; // fused: GATHER_WARPS * GPASS products
-    int32_t* grp;     // fused: GATHER_WARPS * (rows per gather warp + 1) row pointers
+    int32_t* grp;     // fused: GATHER_WARPS * (TILE + 1) row pointers
     uint64_t* full;
     uint64_t* empty;
-    uint64_t* rs_full;   // fused: a tile's sums are ready (GATHER_WARPS arrivals)
+    uint64_t* rs_full;   // fused: a tile's sums are in y (its gather warp's arrival)
     uint64_t* rs_empty;  // fused: the consumers have read them (CONSUMER_WARPS arrivals)
 };
 
@@ -210,15 +205,14 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int R, int nstage, in
     s.scratch = s.ring + (size_t)nstage * ring_stride(R);
     s.wsum = s.scratch + (has_rest ? CONSUMER_WARPS * WPASS : 0);
     double* d = s.wsum + 2 * CONSUMER_WARPS;
-    s.rsum = d;
-    s.gscratch = d + (fused ? RS_BUFS * CONSUMERS * R : 0);
+    s.gscratch = d;
     d = s.gscratch + (fused ? GATHER_WARPS * GPASS : 0);
     s.grp = reinterpret_cast<int32_t*>(d);
     unsigned char* u = reinterpret_cast<unsigned char*>(d) + (fused ? fused_int_bytes(R) : 0);
     s.full = reinterpret_cast<uint64_t*>(u);
     s.empty = s.full + nstage;
     s.rs_full = s.empty + nstage;
-    s.rs_empty = s.rs_full + RS_BUFS;
+    s.rs_empty = s.rs_full + RS_SLOTS;
     return s;
 }
 
@@ -461,7 +455,7 @@ __device__ __forceinline__ void gather_rest_rows(const TmaArgs& a, int64_t w0, i
 // (slices of odd segments start on an odd slot); 3 / 4 multi-block tiles of
 // bl = 256 / 128 without a remainder, rows interleaved inside each block.
 // REST == 3 (fused): warps 9 .. 9+GATHER_WARPS-1 are gather warps (remainder
-// sums of the tiles ahead into shared memory, RS_BUFS tiles in flight); the
+// sums of whole tiles ahead into y, up to RS_SLOTS tiles in flight); the
 // consumers start each row from its sum.  One CTA per SM: the x gathers need
 // about as many warps in flight as rest_pipe_kernel has (24 per SM).
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
@@ -487,8 +481,8 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
             mbar_init(&S.empty[s], CONSUMER_WARPS);
         }
         if (REST == 3) {
-            for (int s = 0; s < RS_BUFS; ++s) {
-                mbar_init(&S.rs_full[s], GATHER_WARPS);
+            for (int s = 0; s < RS_SLOTS; ++s) {
+                mbar_init(&S.rs_full[s], 1);
                 mbar_init(&S.rs_empty[s], CONSUMER_WARPS);
             }
         }
@@ -499,30 +493,26 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
     if constexpr (REST == 3) {
         if (warp > CONSUMER_WARPS) {
             // -------------------------- gather warps --------------------------
-            constexpr int GROWS = gather_rows_per_warp(R);
+            // Gather warp gw sums the remainder of every GATHER_WARPS-th tile of this
+            // CTA's sequence, the whole tile in one continuous pass pipeline, into y
+            // (the rows' starting values; the consumers add the segments and store
+            // y again, normally while the line is still in L2), then arrives on the
+            // tile's hand-off barrier.  Up to RS_SLOTS tiles ahead of the consumers.
             const int gw = warp - CONSUMER_WARPS - 1;
             double* scratch = S.gscratch + gw * GPASS;
-            int32_t* rps = S.grp + gw * (GROWS + 1);
+            int32_t* rps = S.grp + gw * (TILE + 1);
             const double sc = SCALE ? *a.x_scale : 1.0;
-            int rb = 0;
-            uint32_t rph = 0;
-            bool wrapped = false;
+            int k = 0;  // index among this CTA's non-empty tiles (the consumers count the same)
             for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
                 const Geo g = geo<R, MB, PK>(a, tile);
                 if (g.lo >= g.hi) continue;  // the consumers skip it too
-                if (wrapped) mbar_wait(&S.rs_empty[rb], rph ^ 1u);
-                const int64_t w0 = g.lo + (int64_t)gw * GROWS;
-                const int nrows = (int)max((int64_t)0, min((int64_t)GROWS, g.hi - w0));
-                if (nrows > 0)
-                    gather_rest_rows<SCALE, GROWS / 32>(a, w0, nrows, sc, scratch, rps,
-                                                        S.rsum + rb * (CONSUMERS * R) + gw * GROWS, lane);
+                const int kk = k++;
+                if (kk % GATHER_WARPS != gw) continue;
+                const int slot = kk & (RS_SLOTS - 1);
+                if (kk >= RS_SLOTS) mbar_wait(&S.rs_empty[slot], ((kk / RS_SLOTS) - 1) & 1);
+                gather_rest_rows<SCALE, TILE / 32>(a, g.lo, (int)(g.hi - g.lo), sc, scratch, rps, a.y + g.lo, lane);
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&S.rs_full[rb]);
-                if (++rb == RS_BUFS) {
-                    rb = 0;
-                    rph ^= 1u;
-                    wrapped = true;
-                }
+                if (lane == 0) mbar_arrive(&S.rs_full[slot]);
             }
             return;
         }
@@ -643,8 +633,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
     const int rstride = LAY == 3 ? 64 : LAY == 4 ? 32 : MB ? 1 : CONSUMERS;
     auto lr = [&](int r) { return t0 + rstride * r; };  // local row of its r-th row
     const int64_t xlo_valid = -a.row0, xhi_valid = a.n_cols - a.row0;  // x_local index range
-    int rb = 0;          // REST == 3: remainder-sum buffer of this tile
-    uint32_t rph = 0;
+    int kt = 0;          // REST == 3: index among this CTA's non-empty tiles
     int pe0 = 0, pe1 = 0;  // REST == 1: the next tile's remainder entry range
     auto probe = [&](int tl) {
         pe0 = pe1 = 0;
@@ -671,19 +660,16 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         // already summed into y by rest_kernel (REST 2), or summed by this CTA's
         // gather warps into shared memory (REST 3, remainder-heavy matrices).
         if constexpr (REST == 3) {
-            mbar_wait(&S.rs_full[rb], rph);
-            const double* rs = S.rsum + rb * (CONSUMERS * R);
+            const int slot = kt & (RS_SLOTS - 1);
+            mbar_wait(&S.rs_full[slot], (kt / RS_SLOTS) & 1);
 #pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? rs[lr(r)] : 0.0;
-            // release the buffer once the sums are in registers
+            for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? a.y[g.lo + lr(r)] : 0.0;
+            // release the slot once the sums are in registers
 #pragma unroll
             for (int r = 0; r < R; ++r) asm volatile("" ::"d"(acc[r]));
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.rs_empty[rb]);
-            if (++rb == RS_BUFS) {
-                rb = 0;
-                rph ^= 1u;
-            }
+            if (lane == 0) mbar_arrive(&S.rs_empty[slot]);
+            ++kt;
         } else if constexpr (REST == 2) {
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = lr(r) < rows ? a.y[g.lo + lr(r)] : 0.0;
