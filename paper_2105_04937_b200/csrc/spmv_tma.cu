@@ -173,10 +173,11 @@ __device__ __forceinline__ Geo geo(const TmaArgs& a, int tile) {
 __host__ __device__ constexpr int ring_stride(int R) { return CONSUMERS * R + 2; }
 
 // has_rest: the consumers' per-warp remainder scratch (CONSUMER_WARPS * WPASS doubles)
-// fused: the gather warps' product scratch and staged row pointers (each gather
-// warp sums whole tiles: TILE + 1 row pointers), the tile hand-off barriers
-__host__ __device__ inline size_t fused_int_bytes(int R) {
-    return ((size_t)GATHER_WARPS * (CONSUMERS * R + 1) * sizeof(int32_t) + 15) & ~size_t(15);
+// fused: the gather warps' product scratch and staged row pointers (a gather
+// warp sums its tiles in chunks of GCHUNK rows), the tile hand-off barriers
+constexpr int GCHUNK = 256;
+__host__ __device__ inline size_t fused_int_bytes(int) {
+    return ((size_t)GATHER_WARPS * (GCHUNK + 1) * sizeof(int32_t) + 15) & ~size_t(15);
 }
 __host__ __device__ inline size_t smem_bytes(int R, int nstage, int has_rest, int fused = 0) {
     size_t b = sizeof(double) * ((size_t)nstage * ring_stride(R) + (has_rest ? CONSUMER_WARPS * WPASS : 0) +
@@ -192,7 +193,7 @@ struct Smem {
     double* scratch;  // CONSUMER_WARPS * WPASS (remainder products) when has_rest
     double* wsum;     // 2 * CONSUMER_WARPS (fused norm: double-buffered warp partials)
     double* gscratch; // fused: GATHER_WARPS * GPASS products
-    int32_t* grp;     // fused: GATHER_WARPS * (TILE + 1) row pointers
+    int32_t* grp;     // fused: GATHER_WARPS * (GCHUNK + 1) row pointers
     uint64_t* full;
     uint64_t* empty;
     uint64_t* rs_full;   // fused: a tile's sums are in y (its gather warp's arrival)
@@ -494,13 +495,13 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         if (warp > CONSUMER_WARPS) {
             // -------------------------- gather warps --------------------------
             // Gather warp gw sums the remainder of every GATHER_WARPS-th tile of this
-            // CTA's sequence, the whole tile in one continuous pass pipeline, into y
+            // CTA's sequence (in 256-row chunks, rest_pipe_kernel's pipeline) into y
             // (the rows' starting values; the consumers add the segments and store
             // y again, normally while the line is still in L2), then arrives on the
             // tile's hand-off barrier.  Up to RS_SLOTS tiles ahead of the consumers.
             const int gw = warp - CONSUMER_WARPS - 1;
             double* scratch = S.gscratch + gw * GPASS;
-            int32_t* rps = S.grp + gw * (TILE + 1);
+            int32_t* rps = S.grp + gw * (GCHUNK + 1);
             const double sc = SCALE ? *a.x_scale : 1.0;
             int k = 0;  // index among this CTA's non-empty tiles (the consumers count the same)
             for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
@@ -510,7 +511,9 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
                 if (kk % GATHER_WARPS != gw) continue;
                 const int slot = kk & (RS_SLOTS - 1);
                 if (kk >= RS_SLOTS) mbar_wait(&S.rs_empty[slot], ((kk / RS_SLOTS) - 1) & 1);
-                gather_rest_rows<SCALE, TILE / 32>(a, g.lo, (int)(g.hi - g.lo), sc, scratch, rps, a.y + g.lo, lane);
+                for (int64_t c0 = g.lo; c0 < g.hi; c0 += GCHUNK)  // rest_pipe_kernel's 256-row runs
+                    gather_rest_rows<SCALE, GCHUNK / 32>(a, c0, (int)min((int64_t)GCHUNK, g.hi - c0), sc, scratch, rps,
+                                                         a.y + c0, lane);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&S.rs_full[slot]);
             }
@@ -1159,8 +1162,11 @@ template <int R, bool SCALE, bool NORM, int REST, int LAY>
 void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = spmv_tma_kernel<R, SCALE, NORM, REST, LAY>;
     static PerDeviceFlag configured;  // per instantiation and device
-    if (!configured.test_and_set(current_device_index()))
+    if (!configured.test_and_set(current_device_index())) {
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        // fused: ~100 KB of the unified 228 KB as shared memory, the rest L1
+        if (REST == 3) HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 44));
+    }
     constexpr int threads = REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS;
     k<<<grid, threads, smem, st>>>(a);
 }
@@ -1353,10 +1359,16 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
             HDCG_LAUNCH_CHECK("spmv_blk_kernel");
             return;
         }
-        if (b.fused) want_ctas = 1;  // 25 warps per CTA: one per SM
+        // fused: 24 warps per CTA, one CTA per SM, and at most ~98 KB of shared
+        // memory -- the rest of the unified 228 KB stays L1, which holds the
+        // gather warps' outstanding x misses (with the whole array as shared
+        // memory the gathers crawled: profiles/r02g_ab_fused_v2.log)
+        if (b.fused) want_ctas = 1;
         const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
         const size_t fixed = smem_bytes(R, 0, b.has_rest, b.fused);
-        const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed : (227 * 1024) / want_ctas - 1024;
+        const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed
+                              : b.fused ? (size_t)98 * 1024
+                                        : (227 * 1024) / want_ctas - 1024;
         b.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
         const size_t smem = smem_bytes(R, b.nstage, b.has_rest, b.fused);
         const int fit = (int)((227 * 1024) / (smem + 1024));
