@@ -1165,7 +1165,9 @@ void launch_one(const TmaArgs& a, int grid, size_t smem, cudaStream_t st) {
     if (!configured.test_and_set(current_device_index())) {
         HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         // fused: ~100 KB of the unified 228 KB as shared memory, the rest L1
-        if (REST == 3) HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 44));
+        if (REST == 3)
+            HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                           std::min(100, (int)((smem + 1023) / 1024 * 100 + 227) / 228)));
     }
     constexpr int threads = REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS;
     k<<<grid, threads, smem, st>>>(a);
@@ -1366,8 +1368,9 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         if (b.fused) want_ctas = 1;
         const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
         const size_t fixed = smem_bytes(R, 0, b.has_rest, b.fused);
+        static const int fused_kb = getenv("HDCG_FUSED_KB") ? atoi(getenv("HDCG_FUSED_KB")) : 98;  // A/B knob
         const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed
-                              : b.fused ? (size_t)98 * 1024
+                              : b.fused ? (size_t)fused_kb * 1024
                                         : (227 * 1024) / want_ctas - 1024;
         b.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
         const size_t smem = smem_bytes(R, b.nstage, b.has_rest, b.fused);
