@@ -1284,7 +1284,7 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     const bool fusable = !blk && m.n_seg > 0;
     // (the fused mode 3 measured 24% of the HBM peak at config 3 against 52% for
     // mode 2 -- its 16 gather warps per SM keep too few gathers in flight -- so it
-    // is selectable, not the default: profiles/r02d_ab_c3_fused_vs_split.log)
+    // is selectable, not the default: profiles/r02d_ab_packed_and_fused.log)
     int mode = req >= 1 && req <= 3 ? req : (heavy ? 2 : 1);
     if (mode == 3 && !fusable) mode = 2;
     const bool split = a.has_rest && mode == 2;
