@@ -1273,19 +1273,19 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         a.prefetch = e ? atoi(e) : (t.blocks_per_tile > 0 ? 1 : 0);
     }
     // Remainder mode (hdcg_set_kernel_policy / HDCG_REST_MODE override the default):
-    // 2 summed first into y by rest_pipe_kernel -- the default for remainder-heavy
-    // matrices (>= 1 entry per 4 rows); 1 loaded from global memory by the
-    // consumers -- the default otherwise; 3 summed by the CTA's gather warps into
-    // shared memory, tiles ahead of the consumers (matrices with segments).  (A producer staging the remainder through the ring
+    // 3 summed into y by the CTA's gather warps, tiles ahead of the consumers --
+    // remainder-heavy (>= 1 entry per 4 rows) M-HDC; 2 summed first into y by
+    // rest_pipe_kernel -- remainder-heavy HDC and CSR; 1 loaded from global
+    // memory by the consumers -- every other matrix.  (A producer staging the remainder through the ring
     // measured 33% at config 3 and was removed: profiles/README.md.)
     static const int env_mode = getenv("HDCG_REST_MODE") ? atoi(getenv("HDCG_REST_MODE")) : 0;
     const int req = g_rest_mode ? g_rest_mode : env_mode;
     const bool heavy = m.nnz_rest * 4 >= m.n_rows;
     const bool fusable = !blk && m.n_seg > 0;
-    // (the fused mode 3 measured 24% of the HBM peak at config 3 against 52% for
-    // mode 2 -- its 16 gather warps per SM keep too few gathers in flight -- so it
-    // is selectable, not the default: profiles/r02d_ab_packed_and_fused.log)
-    int mode = req >= 1 && req <= 3 ? req : (heavy ? 2 : 1);
+    // Mode 3 is the default for remainder-heavy M-HDC (config 3: 0.62-0.65 ms
+    // against 0.68 ms for mode 2, profiles/r02i_ab_fused_smem_sweep.log); HDC
+    // (one block of n rows) measured 3% slower fused than split, so it keeps mode 2.
+    int mode = req >= 1 && req <= 3 ? req : (heavy ? (fusable && m.kind == HDCG_KIND_MHDC ? 3 : 2) : 1);
     if (mode == 3 && !fusable) mode = 2;
     const bool split = a.has_rest && mode == 2;
     a.fused = a.has_rest && mode == 3;

@@ -558,14 +558,16 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     r = info.tile_rows // 256
     b = lambda v: str(v).lower()  # noqa: E731
     if info.packed_stages > 0:  # tile-packed small blocks (pack.cu)
-        rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
-        return (["hdcg::rest_pipe_kernel"] if rest == 2 else []) + [f"hdcg::spmv_tma_kernel<4,{b(scale)},{b(norm)},{rest},5>"]
+        rest = 0 if info.nnz_rest == 0 else (3 if info.nnz_rest * 4 >= info.n_rows else 1)
+        return [f"hdcg::spmv_tma_kernel<4,{b(scale)},{b(norm)},{rest},5>"]
     inside = info.bl >= info.tile_rows  # tiles inside one block, else whole blocks per tile
     mb = not inside and r == 4 and info.bl % 128 == 0
     blk = not inside and r == 1 and 8 <= info.bl < 256 and info.max_seg_per_block <= 16
     if not ((info.bl >= 256 and inside) or mb or blk):
         return [f"hdcg::spmv_kernel<{r},{b(scale)},{b(norm)}>"]
     rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
+    if rest == 2 and info.n_seg > 0 and not blk and info.kind == KIND_MHDC:
+        rest = 3  # gather warps inside the segment kernel
     ks = ["hdcg::rest_pipe_kernel"] if rest == 2 else []
     if rest == 2 and info.n_seg == 0 and not norm:
         return ks  # a CSR: the remainder kernel's sums are y
