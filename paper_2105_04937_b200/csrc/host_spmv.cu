@@ -13,6 +13,7 @@
 // With pinned host buffers H2D and D2H run concurrently (PCIe is full duplex),
 // so a call costs about max(8 n_cols, 8 n_rows) / PCIe bandwidth instead of the sum.
 #include <algorithm>
+#include <cstdlib>
 
 #include "hdcg_internal.cuh"
 
@@ -20,7 +21,15 @@ namespace hdcg {
 
 namespace {
 
-constexpr int PIPE_CHUNKS = 32;
+// Pipeline granularity: pieces of ~32 MB of x (at least 32, at most 256 chunks),
+// so the fill (the first chunk's x) and the drain (the last chunk's y) stay a
+// small part of the PCIe time.  HDCG_PIPE_CHUNKS overrides (A/B).
+int pipe_chunks(int64_t n_cols) {
+    static const int env = getenv("HDCG_PIPE_CHUNKS") ? atoi(getenv("HDCG_PIPE_CHUNKS")) : 0;
+    if (env > 0) return env;
+    const int64_t want = ceil_div(8 * n_cols, (int64_t)32 << 20);
+    return (int)std::min<int64_t>(256, std::max<int64_t>(32, want));
+}
 
 // per tile: highest global column any of its rows reads (-1: none)
 __global__ void tile_xhi_kernel(int64_t n_tiles, int64_t tpb, int64_t bpt, int64_t tile_rows_n, int64_t bl,
@@ -54,7 +63,8 @@ __global__ void tile_xhi_kernel(int64_t n_tiles, int64_t tpb, int64_t bpt, int64
 void plan_pipeline(Matrix* m, cudaStream_t st) {
     const Tiling t = tiling_of(*m);
     const int64_t nt = t.n_tiles;
-    const int64_t per = std::max<int64_t>(1, ceil_div(nt, PIPE_CHUNKS));
+    const int chunks = pipe_chunks(m->n_cols);
+    const int64_t per = std::max<int64_t>(1, ceil_div(nt, chunks));
     m->chunk_blocks.clear();  // holds TILE boundaries of the chunks
     for (int64_t q = 0; q < nt; q += per) m->chunk_blocks.push_back(q);
     m->chunk_blocks.push_back(nt);
@@ -77,7 +87,7 @@ void plan_pipeline(Matrix* m, cudaStream_t st) {
     }
     // x pieces: equal slices of [0, n_cols), 16-byte aligned boundaries
     m->x_pieces.clear();
-    const int64_t np = std::max<int64_t>(1, std::min<int64_t>(PIPE_CHUNKS, m->n_cols));
+    const int64_t np = std::max<int64_t>(1, std::min<int64_t>(chunks, m->n_cols));
     for (int64_t p = 0; p < np; ++p) m->x_pieces.push_back((m->n_cols * p / np) & ~int64_t(1));
     m->x_pieces.push_back(m->n_cols);
     m->pipe_planned = true;

@@ -294,10 +294,15 @@ class SlabRunner:
 
     transport: "p2p" (hdcgpu.PeerBuffer + PeerHalo; the boundary SpMVs store the
     halos), "nccl" (HaloExchange send/recv), "none" (one rank).  init_x(buf) fills
-    the rank's [H | rows | H] x buffer (the halo included)."""
+    the rank's [H | rows | H] x buffer (the halo included).  device / peer_buffer
+    default to the current CUDA device and hdcgpu.PeerBuffer (the CPU tests
+    inject their own to exercise the cross-rank decisions under gloo)."""
 
-    def __init__(self, plan: SlabPlan, rank: int, compute, init_x, transport: str = "p2p"):
+    def __init__(self, plan: SlabPlan, rank: int, compute, init_x, transport: str = "p2p", device=None,
+                 peer_buffer=None):
         self.plan, self.rank, self.compute, self.init_x = plan, rank, compute, init_x
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.peer_buffer = peer_buffer
         self.world = plan.world
         self.pbufs, self.peer = [], None
         self.halo_ok = {}
@@ -311,7 +316,11 @@ class SlabRunner:
                 self.transport = note
 
     def _dev(self):
-        return torch.device("cuda", torch.cuda.current_device())
+        return self.device
+
+    def _sync(self):
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
 
     def release_peer(self):
         """Unmap the neighbours' buffers on every rank before any rank frees its own."""
@@ -319,7 +328,7 @@ class SlabRunner:
             self.peer.close()
         self.peer = None
         if self.world > 1:
-            torch.cuda.synchronize()
+            self._sync()
             dist.barrier()
         for b in self.pbufs:
             b.free()
@@ -330,9 +339,10 @@ class SlabRunner:
         rows, halo = self.plan.rows[self.rank], self.plan.halo
         if p2p:
             err = ""
+            make = self.peer_buffer or H.PeerBuffer
             try:  # local allocation first, agreed on before the collective handle exchange
                 for _ in range(2):
-                    self.pbufs.append(H.PeerBuffer(rows + 2 * halo))
+                    self.pbufs.append(make(rows + 2 * halo))
             except Exception as e:  # noqa: BLE001 - IPC allocation refused on this box
                 err = repr(e)[:120]
             if all_ranks_agree(not err, self._dev()):
@@ -343,9 +353,9 @@ class SlabRunner:
             if err is not None:
                 self.release_peer()
                 return None, f"nccl (peer-memory setup failed: {err or 'on another rank'})"
-            xb, yb = (torch.as_tensor(b, device="cuda") for b in self.pbufs)
+            xb, yb = (torch.as_tensor(b, device=self.device) for b in self.pbufs)
         else:
-            xb, yb = torch.zeros(rows + 2 * halo, dtype=torch.float64, device="cuda"), None
+            xb, yb = torch.zeros(rows + 2 * halo, dtype=torch.float64, device=self.device), None
         xb.zero_()
         self.init_x(xb)
         it = SlabPowerIteration(self.plan, self.rank, self.compute, xb, comm=self.world > 1, y_buf=yb,
@@ -358,7 +368,7 @@ class SlabRunner:
         force_check_failure: treat the p2p check as failed (tests the fallback)."""
         for _ in range(steps):
             self.it.step()
-        torch.cuda.synchronize()
+        self._sync()
         if self.world == 1:
             return
         ok = verify_halos(self.plan, self.rank, self.it.bufs[0])
@@ -369,13 +379,13 @@ class SlabRunner:
             self.transport = "nccl (p2p halo check failed)"
             for _ in range(steps):
                 self.it.step()
-            torch.cuda.synchronize()
+            self._sync()
             self.halo_ok["after_warmup_nccl"] = verify_halos(self.plan, self.rank, self.it.bufs[0])
         dist.barrier()
 
     def check_after(self, key: str = "after_timed"):
         if self.world > 1:
-            torch.cuda.synchronize()
+            self._sync()
             dist.barrier()
             self.halo_ok[key] = verify_halos(self.plan, self.rank, self.it.bufs[0])
 

@@ -145,3 +145,70 @@ def test_matches_global_oracle_power_iteration():
         x = y
     y2, _, _ = run_world(2)
     assert y2.tobytes() == y.tobytes() or np.max(np.abs(y2 - y)) <= 1e-13 * np.max(np.abs(y))
+
+
+class _FakePeerBuffer:
+    """Stand-in for hdcgpu.PeerBuffer: rank 1 cannot allocate peer memory."""
+
+    def __init__(self, count):
+        if dist.get_rank() == 1:
+            raise RuntimeError("cudaIpcGetMemHandle refused (test)")
+        self.count, self.handle = count, b"\0" * 64
+
+    def free(self):
+        pass
+
+
+def _run_runner(rank, world, port_no, steps, transport, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Port
+        from paper_2105_04937_b200.dist import SlabRunner
+        rp, col, val = synth.laplacian7(NX, NY, NZ)
+        n = NX * NY * NZ
+        mh = Port().to_mhdc(rp, col, val, 0.6, BL)
+        halo = NX * NY
+        plan = SlabPlan.make(n, BL, halo, world, unit=NX * NY * 2)
+        row0, rows = plan.row0[rank], plan.rows[rank]
+        x = synth.x_vector(n, 5)
+        g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
+
+        def init_x(buf):
+            buf[g0 - (row0 - halo):g1 - (row0 - halo)] = torch.from_numpy(x[g0:g1])
+
+        runner = SlabRunner(plan, rank, OracleSlab(mh, row0, rows, halo), init_x, transport, device="cpu",
+                            peer_buffer=_FakePeerBuffer)
+        runner.warm(1)
+        for _ in range(steps - 1):
+            runner.it.step()
+        runner.check_after("after")
+        out[rank] = (runner.transport, runner.halos_ok_everywhere(), runner.y_checksum(),
+                     runner.it.bufs[0][halo:halo + rows].numpy().copy(), float(runner.it.red[0]))
+        runner.release_peer()
+    finally:
+        dist.destroy_process_group()
+
+
+def _runner_world(world, transport, steps=3):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_run_runner, args=(world, _free_port(), steps, transport, out), nprocs=world, join=True)
+    return [out[r] for r in range(world)]
+
+
+@pytest.mark.timeout(300)
+def test_runner_peer_setup_failure_falls_back_on_every_rank():
+    """dist.SlabRunner under gloo: rank 1 cannot allocate peer memory, so EVERY rank
+    agrees to fall back to send/recv before the collective handle exchange (no
+    rank left waiting in it); the halo checks pass after the warm-up and at the
+    end; y, ||y|| and the y checksum equal the one-rank run's."""
+    one = _runner_world(1, "nccl")
+    two = _runner_world(2, "p2p")
+    for tr, ok, _, _, _ in two:
+        assert tr.startswith("nccl (peer-memory setup failed"), tr
+        assert ok
+    assert np.concatenate([p[3] for p in two]).tobytes() == one[0][3].tobytes()
+    assert two[0][2] == two[1][2] == one[0][2]
+    assert two[0][4] == two[1][4] == one[0][4]
