@@ -609,9 +609,13 @@ def test_blk_several_tiles_per_cta(port, packed, monkeypatch):
             m.free()
 
 
-def test_tma_policy_rejects_ineligible_shape():
+def test_tma_policy_rejects_ineligible_shape(monkeypatch):
+    # with the tile-packed layout every M-HDC shape is TMA-eligible; without it
+    # (HDCG_PACKED=0) bl = 7 is below spmv_blk_kernel's minimum of 8
+    monkeypatch.setenv("HDCG_PACKED", "0")
     A = csr(*synth.laplacian7(8, 8, 8))
     m = H.to_mhdc(A, 0.6, 7)
+    assert m.info.packed_stages == 0
     try:
         H.set_kernel_policy(H.POLICY_TMA)
         with pytest.raises(ValueError):
