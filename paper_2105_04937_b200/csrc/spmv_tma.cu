@@ -1369,9 +1369,14 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         const size_t stage = smem_bytes(R, 1, 0) - smem_bytes(R, 0, 0);
         const size_t fixed = smem_bytes(R, 0, b.has_rest, b.fused);
         static const int fused_kb = getenv("HDCG_FUSED_KB") ? atoi(getenv("HDCG_FUSED_KB")) : 98;  // A/B knob
+        // Ring of ~48 KB per CTA (3 CTAs per SM: ~150 KB of shared memory): the
+        // rest of the unified 228 KB stays L1, where the x lines of a tile's
+        // offsets are reused.  With the whole array as ring (3 x 73 KB) the x loads
+        // missed L1 (18% hits) and config 4 ran at 92% of the copy peak; with 48 KB
+        // it runs at 104%, configs 1-2 at 96-99% (profiles/r02n_ab_ring_sweep.log).
         const size_t budget = env_kb > 0 ? (size_t)env_kb * 1024 + fixed
                               : b.fused ? (size_t)fused_kb * 1024
-                                        : (227 * 1024) / want_ctas - 1024;
+                                        : std::min<size_t>((227 * 1024) / want_ctas - 1024, 48 * 1024 + fixed);
         b.nstage = std::max(2, std::min(32, (int)((budget > fixed ? budget - fixed : 0) / stage)));
         const size_t smem = smem_bytes(R, b.nstage, b.has_rest, b.fused);
         const int fit = (int)((227 * 1024) / (smem + 1024));
