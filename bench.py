@@ -461,7 +461,7 @@ def run_ours(a):
                          "kernel_ms": round(kern_ms, 4), "peak_source": f"{peak_kind} hbm_gbs",
                          "kernel": kernel_name(info, scale=True, norm=True),
                          "over_ranks": "slowest rank (max kernel time)" if world > 1 else "n/a",
-                         "step_share": "SpMV launches = 99.8% of the step's kernel time (profiles/r01_v18_c4_launches.json)"},
+                         "step_share": "SpMV launches = 99.8% of the step's kernel time (profiles/r02o_c4_launches.json)"},
             "e2e": {"value": round(flops / e2e_s / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h * world, "steps": e2e_steps,
                     "api": "hdcg_spmv_host (pinned host x/y)" if world == 1 else "per-rank H2D+spmv_slab+D2H"},
