@@ -1,0 +1,130 @@
+"""Runs scripts/gather_probe.cu on the GPU box: config-3-like remainder entries
+(6 per row, columns uniform within +-2^16 of the row, n = 2^24) gathered in
+row-major order vs sorted by column inside groups of T rows (products scattered
+into shared memory, summed per row in stored order), and random 8-byte loads from
+a window held in a cluster's distributed shared memory.  Prints one JSON line per
+case: ms, entries per cycle per SM (at 1965 MHz), GB/s of the (col, dest, val)
+streams."""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+L = ctypes.CDLL(os.path.join(HERE, "libgather_probe.so"))
+P = ctypes.c_void_p
+L.gp_probe.argtypes = [P, P, P, P, P] + [ctypes.c_int] * 8 + [P]
+L.gp_pure.argtypes = [P, P] + [ctypes.c_int] * 6 + [P]
+L.gp_dsmem.argtypes = [P, P] + [ctypes.c_int] * 5 + [P]
+dev = torch.device("cuda")
+n = 1 << 24
+per_row = 6
+g = torch.Generator(device=dev)
+g.manual_seed(4)
+x = torch.rand(n, dtype=torch.float64, device=dev, generator=g) * 2 - 1
+rows = torch.arange(n, device=dev, dtype=torch.int64).repeat_interleave(per_row)
+col = (rows + torch.randint(-(1 << 16), 1 << 16, (n * per_row,), device=dev, generator=g)).clamp_(0, n - 1)
+val = torch.rand(n * per_row, dtype=torch.float64, device=dev, generator=g)
+y_ref = (val * x[col]).view(n, per_row)
+acc = torch.zeros(n, dtype=torch.float64, device=dev)
+for k in range(per_row):
+    acc = acc + y_ref[:, k]
+y_ref = acc
+flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+stream = torch.cuda.current_stream().cuda_stream
+
+
+def timed(fn, reps=5):
+    best = 1e9
+    for i in range(reps + 2):
+        flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        rc = fn()
+        e.record()
+        torch.cuda.synchronize()
+        assert rc == 0, rc
+        if i >= 2:
+            best = min(best, s.elapsed_time(e))
+    return best
+
+
+def case(T, order, nt, u, dmod=0):
+    ng = n // T
+    dmod = dmod or ng
+    epg = T * per_row
+    pos = torch.arange(n * per_row, device=dev, dtype=torch.int64)
+    if order == "sorted":
+        key = (rows // T) * (1 << 22) + (col - (rows // T) * T + (1 << 17))
+        perm = torch.sort(key).indices
+        del key
+    elif order == "sorted_lines":   # sorted by 128-byte line only, row-major inside a line
+        key = ((rows // T) * (1 << 22) + (col - (rows // T) * T + (1 << 17)) // 16) * (1 << 20) + pos % epg
+        perm = torch.sort(key).indices
+        del key
+    else:
+        perm = pos
+    c = (col - (rows // T) * T + (1 << 16))[perm].to(torch.int32).contiguous()
+    d = (pos[perm] % epg).to(torch.int16).contiguous()   # bit pattern of uint16 (epg < 65535)
+    v = val[perm].contiguous()
+    y = torch.zeros(n, dtype=torch.float64, device=dev)
+    fn = lambda: L.gp_probe(c.data_ptr(), d.data_ptr(), v.data_ptr(), x.data_ptr(), y.data_ptr(), T, per_row, ng,
+                            dmod, n, 148, nt, u, stream)
+    ms = timed(fn)
+    ok = bool(torch.equal(y, y_ref)) if dmod == ng else None
+    ents = n * per_row
+    print(json.dumps({"T": T, "order": order, "dmod": dmod, "nt": nt, "u": u, "ms": round(ms, 4), "bitwise": ok,
+                      "entries_per_cycle_sm": round(ents / (ms * 1e-3) / 1.965e9 / 148, 3),
+                      "stream_gbs": round(ents * 14 / (ms * 1e-3) / 1e9, 1)}), flush=True)
+
+
+def dsmem(csize, per, u):
+    grid = (148 // csize) * csize
+    iters = 64
+    idx = torch.randint(0, per * csize, (grid * 1024 * u * iters,), device=dev, dtype=torch.int32)
+    out = torch.zeros(grid * 1024, dtype=torch.float64, device=dev)
+    fn = lambda: L.gp_dsmem(idx.data_ptr(), out.data_ptr(), per, iters, grid, csize, u, stream)
+    ms = timed(fn)
+    loads = grid * 1024 * u * iters
+    print(json.dumps({"dsmem_cluster": csize, "per_cta_kb": per * 8 // 1024, "u": u, "ms": round(ms, 4),
+                      "loads_per_cycle_sm": round(loads / (ms * 1e-3) / 1.965e9 / grid, 3)}), flush=True)
+
+
+def pure(K, u, grid, wbits=17):
+    iters = 2048 // u
+    out = torch.zeros(grid * 1024, dtype=torch.float64, device=dev)
+    fn = lambda: L.gp_pure(x.data_ptr(), out.data_ptr(), iters, K, n, wbits, u, grid, stream)
+    ms = timed(fn)
+    loads = grid * 1024 * u * iters
+    print(json.dumps({"pure_gather_lanes_per_line": K, "u": u, "grid": grid, "window_bits": wbits, "ms": round(ms, 4),
+                      "loads_per_cycle_sm": round(loads / (ms * 1e-3) / 1.965e9 / 148, 3),
+                      "ms_per_103.6M": round(ms * 103.6e6 / loads, 4),
+                      "sector_gbs_if_1_per_load": round(loads * 32 / (ms * 1e-3) / 1e9, 1)}), flush=True)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["pure", "l2", "streams", "dsmem"]
+    if "pure" in which:      # the chip's random-gather rate: no index streams
+        for K in (1, 2, 4, 8):
+            for u in (4, 8, 16):
+                for grid in (148, 296):
+                    pure(K, u, grid)
+        pure(1, 8, 296, wbits=13)
+        pure(1, 8, 296, wbits=20)
+    if "l2" in which:        # entry streams L2-resident: the gather + scatter + row-sum structure alone
+        for T in (1024, 2048, 4096):
+            for order in ("rowmajor", "sorted"):
+                for nt, u in ((1024, 4), (1024, 8)):
+                    case(T, order, nt, u, dmod=148)
+        case(4096, "sorted_lines", 1024, 4, dmod=148)
+    if "streams" in which:   # entry streams from DRAM
+        for T in (1024, 2048, 4096):
+            for order in ("rowmajor", "sorted"):
+                for nt, u in ((1024, 4), (1024, 8), (512, 8)):
+                    case(T, order, nt, u)
+    if "dsmem" in which:
+        for csize in (8, 4, 2, 1):
+            for u in (4, 8):
+                dsmem(csize, 17408, u)
