@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libhdcgpu.so")
-SOURCES = ["spmv.cu", "spmv_tma.cu", "convert.cu", "pack.cu", "analyze.cu", "host_spmv.cu", "membench.cu",
+SOURCES = ["spmv.cu", "spmv_tma.cu", "spmv_rows.cu", "convert.cu", "pack.cu", "analyze.cu", "host_spmv.cu", "membench.cu",
            "mmio.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -102,6 +102,7 @@ void stage_csr(Staged& s, int64_t n_rows, int64_t n_cols, int64_t row0, int64_t 
 }
 
 void account(Matrix* m) {
+    rest_run_stats(m);
     m->device_bytes = sizeof(int32_t) * (m->n_blocks + 1 + m->n_seg + m->n_rows + 1 + m->nnz_rest) +
                       sizeof(double) * (m->n_seg * m->bl + m->nnz_rest);
     if (m->packed) m->device_bytes += sizeof(double) * m->pk_stages * PACK_TILE;  // + small tables

@@ -1,0 +1,283 @@
+// spmv_rows.cu -- remainder / CSR row sums with one row per lane and the entry
+// streams staged through shared memory by TMA (sm_100a).
+//
+// The reference sums a row's remainder entries in stored order onto +0.0
+// (kernels.cpp:39-60 spmv_csr, :192-197 the M-HDC remainder).  rest_pipe_kernel
+// (spmv_tma.cu) keeps that order with entry-major lanes: 32 lanes load 32
+// consecutive entries, gather x, and pass the products through shared memory to
+// the lane that owns the row.  For structured rows (a stencil stored as CSR: 27
+// consecutive entries are 27 different x lines) every warp gather touches ~32
+// lines, and the kernel is bound by L1 wavefronts (config 2 as CSR: 68% of the
+// HBM peak), not by bytes.
+//
+// Here a lane owns a row and walks its entries in order (the reference's loop,
+// no product hand-off), so the k-th gathers of 32 adjacent rows are adjacent
+// columns for banded matrices: 2-3 lines per warp gather.  Column indices and
+// values never touch L1: a producer warp streams the CTA's contiguous entry range
+// through a ring of CAP-entry stages with cp.async.bulk (L2 evict-first), and the
+// lanes read them from shared memory (stride = row length: conflict-free for odd
+// lengths).  Each CTA owns a contiguous range of 32-row runs (one wave, static
+// partition); consumer warp w takes runs w, w + W, ... of it.  Ring protocol:
+// every consumer warp passes every stage in stream order -- it waits for the
+// stage's full barrier and, once its next run starts beyond the stage, arrives on
+// the stage's empty barrier (W arrivals free the slot).  A run's entries must be
+// resident together, so the matrix is eligible when its longest 32-row run fits
+// the ring with a stage to spare (Matrix::rest_run_max, measured at build time);
+// other matrices keep rest_pipe_kernel.
+//
+// Same per-row operations in the same order as warp_rest / rest_pipe_kernel:
+// acc = __dadd_rn(acc, __dmul_rn(v, x[c] (* scale))) from +0.0 -- bitwise equal.
+#include <algorithm>
+#include <cstdlib>
+
+#include "hdcg_internal.cuh"
+#include "tma_ptx.cuh"
+
+namespace hdcg {
+
+namespace {
+
+#ifndef HDCG_ROWS_W16_CTAS
+#define HDCG_ROWS_W16_CTAS 2
+#endif
+constexpr int CAP_LOG2 = 10;
+constexpr int CAP = 1 << CAP_LOG2;  // entries per ring stage: 4 KB of columns + 8 KB of values
+#ifndef HDCG_ROWS_UNROLL
+#define HDCG_ROWS_UNROLL 9  // 27-point rows: three full batches (8: 75%, 9: 81% of the HBM peak at config 2 as CSR)
+#endif
+constexpr int UNROLL = HDCG_ROWS_UNROLL;  // x gathers in flight per lane
+
+struct RowsArgs {
+    const int32_t* rp;
+    const int32_t* col;  // padded: readable up to a multiple of 4 entries past the end
+    const double* val;
+    const double* x;  // x_local: x[c - row0]
+    double* y;
+    const double* x_scale;
+    int64_t row0;
+    int64_t r_lo, r_hi;  // local rows
+    int prefetch;        // stages the producer pulls into L2 ahead of the ring (0: none)
+    int ns_log2;         // ring stages = 1 << ns_log2 (shifts, no divisions, in the stage bookkeeping)
+};
+
+template <int W, bool SCALE>
+__global__ void __launch_bounds__(32 * (W + 1), W >= 16 ? HDCG_ROWS_W16_CTAS : 2) rest_rows_kernel(const RowsArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int NSL = a.ns_log2, NS = 1 << NSL;
+    const int ring = NS << CAP_LOG2, mask = ring - 1;
+    double* sval = reinterpret_cast<double*>(smem_raw);
+    int32_t* scol = reinterpret_cast<int32_t*>(sval + ring);
+    uint64_t* full = reinterpret_cast<uint64_t*>(scol + ring);
+    uint64_t* empty = full + NS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // this CTA's contiguous range of 32-row runs
+    const int64_t n_runs = (a.r_hi - a.r_lo + 31) >> 5;
+    const int64_t per = (n_runs + gridDim.x - 1) / gridDim.x;
+    const int64_t g_lo = (int64_t)blockIdx.x * per, g_hi = min(g_lo + per, n_runs);
+    if (g_lo >= g_hi) return;
+    const int64_t R0 = a.r_lo + (g_lo << 5), R1 = min(a.r_lo + (g_hi << 5), a.r_hi);
+    const int64_t E0 = __ldg(a.rp + R0), E1 = __ldg(a.rp + R1);
+    const int64_t E0a = E0 & ~int64_t(3);  // 16-byte aligned column window
+    const int NQ = E1 > E0 ? (int)((E1 - E0a + CAP - 1) >> CAP_LOG2) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, W);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == W) {  // producer: the entry stream, stage by stage
+        if (lane == 0) {
+            const uint64_t pol = evict_first_policy();
+            const int64_t E1a = (E1 + 3) & ~int64_t(3);
+            const int PF = a.prefetch;
+            auto prefetch_stage = [&](int q) {  // DRAM -> L2, far ahead of the ring
+                const int64_t e = E0a + ((int64_t)q << CAP_LOG2);
+                const uint32_t cnt = (uint32_t)min((int64_t)CAP, E1a - e);
+                bulk_prefetch_l2(a.col + e, cnt * 4u);
+                bulk_prefetch_l2(a.val + e, cnt * 8u);
+            };
+            if (PF > 0)
+                for (int q = NS; q < min(NQ, NS + PF); ++q) prefetch_stage(q);
+            for (int q = 0; q < NQ; ++q) {
+                const int s = q & (NS - 1);
+                if (PF > 0 && q + NS + PF < NQ) prefetch_stage(q + NS + PF);
+                if (q >= NS) mbar_wait(empty + s, (uint32_t)(((q >> NSL) - 1) & 1));
+                const int64_t e = E0a + ((int64_t)q << CAP_LOG2);
+                const uint32_t cnt = (uint32_t)min((int64_t)CAP, E1a - e);
+                mbar_expect_tx(full + s, cnt * 12u);
+                bulk_g2s(scol + ((size_t)s << CAP_LOG2), a.col + e, cnt * 4u, full + s, pol);
+                bulk_g2s(sval + ((size_t)s << CAP_LOG2), a.val + e, cnt * 8u, full + s, pol);
+            }
+        }
+        return;
+    }
+
+    const double sc = SCALE ? *a.x_scale : 1.0;
+    int passed = 0;  // stages [0, passed) waited for and released by this warp
+    int64_t g = g_lo + warp;
+    // this run's row pointers; the next run's are loaded while this one is summed
+    int kb = 0, ke = 0;
+    if (g < g_hi) {
+        const int64_t row = a.r_lo + (g << 5) + lane;
+        kb = __ldg(a.rp + min(row, R1));
+        ke = __ldg(a.rp + min(row + 1, R1));
+    }
+    for (; g < g_hi; g += W) {
+        const int64_t row = a.r_lo + (g << 5) + lane;
+        int kb_n = 0, ke_n = 0;
+        if (g + W < g_hi) {
+            const int64_t rn = row + ((int64_t)W << 5);
+            kb_n = __ldg(a.rp + min(rn, R1));
+            ke_n = __ldg(a.rp + min(rn + 1, R1));
+        }
+        const int ea = __shfl_sync(0xffffffffu, kb, 0), eb = __shfl_sync(0xffffffffu, ke, 31);
+        double acc = 0.0;
+        if (eb > ea) {
+            const int qa = (int)((ea - E0a) >> CAP_LOG2), qb = (int)((eb - 1 - E0a) >> CAP_LOG2);
+            for (; passed < qa; ++passed) {  // stages of the other warps' runs
+                const int s = passed & (NS - 1);
+                mbar_wait(full + s, (uint32_t)((passed >> NSL) & 1));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty + s);
+            }
+            for (int q = qa; q <= qb; ++q) mbar_wait(full + (q & (NS - 1)), (uint32_t)((q >> NSL) & 1));
+            const int base = (int)E0a;
+            for (int p = kb; p < ke; p += UNROLL) {
+                int32_t c[UNROLL];
+                double v[UNROLL], xv[UNROLL];
+#pragma unroll
+                for (int j = 0; j < UNROLL; ++j) {
+                    const int i = (p + j - base) & mask;
+                    const bool ok = p + j < ke;
+                    c[j] = ok ? scol[i] : -1;
+                    v[j] = ok ? sval[i] : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < UNROLL; ++j) xv[j] = c[j] >= 0 ? __ldg(a.x + ((int64_t)c[j] - a.row0)) : 0.0;
+#pragma unroll
+                for (int j = 0; j < UNROLL; ++j) {
+                    double t = xv[j];
+                    if (SCALE) t = __dmul_rn(t, sc);
+                    if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], t));
+                }
+            }
+        }
+        if (row < R1) a.y[row] = acc;
+        kb = kb_n;
+        ke = ke_n;
+    }
+    // let the producer finish the stream for the warps still at work
+    __syncwarp();
+    for (; passed < NQ; ++passed) {
+        const int s = (int)(passed & (NS - 1));
+        mbar_wait(full + s, (uint32_t)((passed >> NSL) & 1));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+    }
+}
+
+__global__ void run_max_kernel(const int32_t* __restrict__ rp, int64_t n_rows, int* out) {
+    const int64_t n_runs = (n_rows + 31) >> 5;
+    int mx = 0;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_runs; g += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, rp[min((g + 1) << 5, n_rows)] - rp[g << 5]);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(out, mx);
+}
+
+template <int W, bool SCALE>
+void launch_rows(const RowsArgs& a, int grid, size_t smem, cudaStream_t st) {
+    auto k = rest_rows_kernel<W, SCALE>;
+    static PerDeviceFlag configured;
+    if (!configured.test_and_set(current_device_index()))
+        HDCG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    k<<<grid, 32 * (W + 1), smem, st>>>(a);
+}
+
+}  // namespace
+
+// The longest remainder run (entries of 32 consecutive rows, 32-aligned), measured
+// once when the matrix is built: selects rest_rows_kernel (spmv_rows.cu).
+void rest_run_stats(Matrix* m) {
+    m->rest_run_max = 0;
+    if (m->nnz_rest <= 0 || m->n_rows <= 0) return;
+    DeviceGuard dg(m->device);
+    int* d = dev_alloc<int>(1, nullptr);
+    HDCG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), nullptr));
+    run_max_kernel<<<grid_cap(ceil_div(ceil_div(m->n_rows, 32), 256)), 256>>>(m->rest_rp, m->n_rows, d);
+    HDCG_LAUNCH_CHECK("run_max_kernel");
+    int v = 0;
+    HDCG_CUDA(cudaMemcpy(&v, d, sizeof(int), cudaMemcpyDeviceToHost));
+    dev_free(d, nullptr);
+    m->rest_run_max = v;
+}
+
+// Remainder sums of local rows [r0, r1) into y (from +0.0).  False when the matrix
+// is not eligible (a 32-row run longer than the ring holds) or the arrays are not
+// 16-byte aligned: the caller then uses rest_pipe_kernel.
+// HDCG_ROWS_W (8 | 16 consumer warps) and HDCG_ROWS_STAGES (ring stages of 1024
+// entries, a power of two <= 16) are A/B knobs.
+bool rest_rows_launch(const Matrix& m, const double* x_local, double* y, const double* x_scale, int64_t r0,
+                      int64_t r1, cudaStream_t st) {
+    if (r1 <= r0) return true;
+    if (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0) return false;
+    const char* ew = getenv("HDCG_ROWS_W");  // read per call: the tests switch them in-process
+    const char* es = getenv("HDCG_ROWS_STAGES");
+    const int env_w = ew ? atoi(ew) : 0, env_ns = es ? atoi(es) : 0;
+    const char* ep = getenv("HDCG_ROWS_PF");
+    // runs of a launch start at r0, which need not be 32-aligned: a window of 32
+    // rows overlaps at most two aligned runs
+    const int64_t run_max = 2 * m.rest_run_max;
+    // Default: rows of >= 16 entries on average (a 27-point stencil as CSR: 864
+    // entries per run) take 16 warps and a 16-stage (192 KB) ring, one CTA per SM:
+    // config 2 as CSR 68% -> 81% of the HBM peak.  Short rows stay on
+    // rest_pipe_kernel, whose entry-major lanes keep more gathers in flight
+    // (config 1 as CSR 81% vs 79% here; config 3's random columns 61% vs 31%:
+    // profiles/r02s_ab_rows.log).  The knobs force this kernel (tests, A/B).
+    const int64_t avg_run = m.nnz_rest * 32 / std::max<int64_t>(1, m.n_rows);
+    if (!env_w && !env_ns && avg_run * 16 <= 8 * CAP) return false;
+    int W = env_w ? env_w : 16;
+    int NS = env_ns ? env_ns : 16;
+    if (W != 8 && W != 16) return false;
+    if (NS < 2 || (NS & (NS - 1)) || NS > 16) return false;
+    if (run_max > (int64_t)(NS - 1) * CAP) {
+        if (env_ns) return false;
+        NS = 16;  // the larger ring, if that holds the longest run
+        if (run_max > (int64_t)(NS - 1) * CAP) return false;
+    }
+    RowsArgs a;
+    a.rp = m.rest_rp;
+    a.col = m.rest_col;
+    a.val = m.rest_val;
+    a.x = x_local;
+    a.y = y;
+    a.x_scale = x_scale;
+    a.row0 = m.row0;
+    a.r_lo = r0;
+    a.r_hi = r1;
+    a.prefetch = ep ? atoi(ep) : 0;  // measured slower with any look-ahead (profiles/r02s_ab_rows.log)
+    a.ns_log2 = 0;
+    while ((1 << a.ns_log2) < NS) ++a.ns_log2;
+    const size_t smem = (size_t)NS * CAP * 12 + sizeof(uint64_t) * 2 * NS;
+    const int per_sm = std::max(1, std::min(2, (int)((227 * 1024) / (smem + 1024))));
+    const int64_t n_runs = ceil_div(r1 - r0, 32);
+    // at least 4 runs per consumer warp and CTA: small row ranges take fewer CTAs
+    const int64_t want = std::max<int64_t>(1, n_runs / (4 * W));
+    const int grid = (int)std::min<int64_t>((int64_t)sm_count() * per_sm, want);
+    if (W == 16) {
+        if (x_scale) launch_rows<16, true>(a, grid, smem, st);
+        else launch_rows<16, false>(a, grid, smem, st);
+    } else {
+        if (x_scale) launch_rows<8, true>(a, grid, smem, st);
+        else launch_rows<8, false>(a, grid, smem, st);
+    }
+    HDCG_LAUNCH_CHECK("rest_rows_kernel");
+    return true;
+}
+
+}  // namespace hdcg

@@ -39,6 +39,7 @@
 #include <cstdlib>
 
 #include "hdcg_internal.cuh"
+#include "tma_ptx.cuh"
 
 namespace hdcg {
 
@@ -59,43 +60,6 @@ constexpr int GPER = 8;                  // x gathers per lane per pass
 constexpr int GPASS = 32 * GPER;         // entries per gather-warp pass
 constexpr int RS_SLOTS = 2 * 32;         // tile hand-off barriers (>= 2 * GATHER_WARPS, power of 2)
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-        : "memory");
-}
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONSUMERS) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -1297,9 +1261,10 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
         tile_rows(te - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m.bl, m.n_rows, &dummy, &r1);
         r0 = std::min(r0, m.n_rows);
         if (r1 <= r0) return;
-        // HDCG_REST_VARIANT: A/B knob, read per call (tests switch it in-process)
+        // HDCG_REST_VARIANT: A/B knob, read per call (tests switch it in-process):
+        // 0 rest_kernel, 1-4 rest_pipe_kernel shapes, 5 (default) rest_rows_kernel
         const char* ev = getenv("HDCG_REST_VARIANT");
-        const int variant = ev ? atoi(ev) : 1;
+        const int variant = ev ? atoi(ev) : 5;
         auto pipe = [&](auto kern, int g) {
             kern<<<(unsigned)ceil_div(r1 - r0, (int64_t)CONSUMERS * g), CONSUMERS, 0, s>>>(a, r0, r1);
         };
@@ -1322,6 +1287,9 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
                 if (x_scale) pipe(rest_pipe_kernel<true, 3, 16, 8>, 16);
                 else pipe(rest_pipe_kernel<false, 3, 16, 8>, 16);
                 break;
+            case 5:  // one row per lane, entry streams staged by TMA (spmv_rows.cu), when eligible
+                if (rest_rows_launch(m, x_local, y, x_scale, r0, r1, s)) break;
+                [[fallthrough]];
             default:
                 if (x_scale) pipe(rest_pipe_kernel<true, 3, 8, 8>, 8);
                 else pipe(rest_pipe_kernel<false, 3, 8, 8>, 8);

@@ -316,7 +316,33 @@ def test_config2_27pt(port):
     assert m.n_segments == 46494
     y = H.spmv_mhdc(m, x)
     assert y.tobytes() == port.spmv_mhdc(ref, x, 0).tobytes()
-    assert_within_tol(y, port.spmv_csr(rp, col, val, x, 0), rp, col, val, x)
+    yc = port.spmv_csr(rp, col, val, x, 0)
+    assert_within_tol(y, yc, rp, col, val, x)
+    # as a CSR (27 entries per row): the default path is rest_rows_kernel (one row per
+    # lane, TMA-staged entry ring) -- whole matrix, then a block sub-range of the
+    # all-remainder M-HDC (theta = 1 selects nothing) with the x scale and the tile norm
+    assert "rest_rows_kernel" in " ".join(H.spmv_kernels(H.device_csr(A).info))
+    assert H.spmv_csr(A, x).tobytes() == yc.tobytes()
+    # theta = 1 keeps only the completely filled segments: two thirds of the entries
+    # stay in the remainder (>= 16 per row); split mode sums them with rest_rows_kernel
+    m1 = H.to_mhdc(A, 1.0, 4096)
+    ref1 = port.to_mhdc(rp, col, val, 1.0, 4096)
+    assert m1.info.nnz_rest * 2 >= m1.info.n_rows * 32
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.zeros(n, dtype=torch.float64, device="cuda")
+    tiles = torch.zeros(m1.info.n_tiles, dtype=torch.float64, device="cuda")
+    sc = torch.tensor([0.25], dtype=torch.float64, device="cuda")
+    b0, b1 = 3, m1.n_blocks - 5
+    H.set_kernel_policy(H.POLICY_TMA, H.REST_SPLIT)
+    try:
+        H.spmv_slab(m1, xd.data_ptr(), yd.data_ptr(), b0, b1, sc.data_ptr(), tiles.data_ptr())
+        torch.cuda.synchronize()
+    finally:
+        H.set_kernel_policy(H.POLICY_AUTO)
+    want = port.spmv_mhdc(ref1, x * 0.25, 0)
+    got = yd.cpu().numpy()
+    assert got[b0 * 4096:b1 * 4096].tobytes() == want[b0 * 4096:b1 * 4096].tobytes()
+    assert not got[:b0 * 4096].any() and not got[b1 * 4096:].any()
 
 
 def test_config3_quasi_diagonal(port):
@@ -941,14 +967,22 @@ def test_peer_halo_power_iteration_two_processes(tmp_path, transport):
     assert tr == {"p2p": "p2p", "sendrecv": "nccl", "p2p_fallback": "nccl (p2p halo check failed)"}[transport]
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5", "5/16/16", "5/8/2", "5/8/16"])
 def test_remainder_kernel_variants_and_csr(port, variant, monkeypatch):
     """Every remainder-sum kernel variant (HDCG_REST_VARIANT: 0 rest_kernel, 1-4
-    the software-pipelined rest_pipe_kernel with several run/pass sizes) is bitwise
-    equal to the oracle: M-HDC with a heavy remainder, and pure CSR (no segments:
-    the remainder kernel's sums are y) with skewed row lengths -- empty rows, rows
-    longer than a pass, partial warp ranges -- plain and in power-iteration form."""
+    the software-pipelined rest_pipe_kernel with several run/pass sizes, 5 the
+    row-per-lane rest_rows_kernel with its TMA-staged entry ring -- default shape,
+    16 warps, a 2-stage and a 16-stage ring) is bitwise equal to the oracle: M-HDC
+    with a heavy remainder, and pure CSR (no segments: the remainder kernel's sums
+    are y) with skewed row lengths -- empty rows, rows longer than a pass, a row
+    longer than the ring (falls back to rest_pipe_kernel), partial warp ranges --
+    plain and in power-iteration form."""
+    variant, _, shape = variant.partition("/")
     monkeypatch.setenv("HDCG_REST_VARIANT", variant)
+    if shape:
+        w, ns = shape.split("/")
+        monkeypatch.setenv("HDCG_ROWS_W", w)
+        monkeypatch.setenv("HDCG_ROWS_STAGES", ns)
     H.set_kernel_policy(H.POLICY_TMA, H.REST_SPLIT)
     try:
         _remainder_cases(port)
@@ -959,6 +993,8 @@ def test_remainder_kernel_variants_and_csr(port, variant, monkeypatch):
             lens[rng.random(n) < 0.2] = 0
             if n > 100:
                 lens[rng.integers(0, n, 4)] = rng.integers(300, 3000, 4)
+            if n > 70000:
+                lens[12345] = 20000  # longer than any ring of rest_rows_kernel
             rows = np.repeat(np.arange(n), lens)
             cols = rng.integers(0, n, rows.size)
             vals = rng.uniform(-1, 1, rows.size)
