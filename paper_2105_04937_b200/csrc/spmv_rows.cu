@@ -56,7 +56,7 @@ struct RowsArgs {
     const double* x_scale;
     int64_t row0;
     int64_t r_lo, r_hi;  // local rows
-    int prefetch;        // stages the producer pulls into L2 ahead of the ring (0: none)
+    int chunk_runs;      // 32-row runs per chunk (chunks are dealt round-robin to the CTAs)
     int ns_log2;         // ring stages = 1 << ns_log2 (shifts, no divisions, in the stage bookkeeping)
 };
 
@@ -71,15 +71,16 @@ __global__ void __launch_bounds__(32 * (W + 1), W >= 16 ? HDCG_ROWS_W16_CTAS : 2
     uint64_t* empty = full + NS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    // this CTA's contiguous range of 32-row runs
+    // Chunks of K 32-row runs, dealt round-robin to the CTAs: the CTAs at work at any
+    // time cover one contiguous stretch of rows, so their x windows overlap in L2 (a
+    // contiguous range per CTA spread 296 windows over the whole vector: config 3 as
+    // CSR read 2.1x its bytes from DRAM, profiles/r02u_c3csr_rows_contig_ncu.json).
+    // The ring runs on across chunks: stage numbers are global, chunk c's first
+    // stage is q_base (every warp derives the same counts from the row pointers).
     const int64_t n_runs = (a.r_hi - a.r_lo + 31) >> 5;
-    const int64_t per = (n_runs + gridDim.x - 1) / gridDim.x;
-    const int64_t g_lo = (int64_t)blockIdx.x * per, g_hi = min(g_lo + per, n_runs);
-    if (g_lo >= g_hi) return;
-    const int64_t R0 = a.r_lo + (g_lo << 5), R1 = min(a.r_lo + (g_hi << 5), a.r_hi);
-    const int64_t E0 = __ldg(a.rp + R0), E1 = __ldg(a.rp + R1);
-    const int64_t E0a = E0 & ~int64_t(3);  // 16-byte aligned column window
-    const int NQ = E1 > E0 ? (int)((E1 - E0a + CAP - 1) >> CAP_LOG2) : 0;
+    const int K = a.chunk_runs;
+    const int64_t n_chunks = (n_runs + K - 1) / K;
+    if ((int64_t)blockIdx.x >= n_chunks) return;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -90,94 +91,116 @@ __global__ void __launch_bounds__(32 * (W + 1), W >= 16 ? HDCG_ROWS_W16_CTAS : 2
     }
     __syncthreads();
 
-    if (warp == W) {  // producer: the entry stream, stage by stage
-        if (lane == 0) {
-            const uint64_t pol = evict_first_policy();
-            const int64_t E1a = (E1 + 3) & ~int64_t(3);
-            const int PF = a.prefetch;
-            auto prefetch_stage = [&](int q) {  // DRAM -> L2, far ahead of the ring
-                const int64_t e = E0a + ((int64_t)q << CAP_LOG2);
-                const uint32_t cnt = (uint32_t)min((int64_t)CAP, E1a - e);
-                bulk_prefetch_l2(a.col + e, cnt * 4u);
-                bulk_prefetch_l2(a.val + e, cnt * 8u);
-            };
-            if (PF > 0)
-                for (int q = NS; q < min(NQ, NS + PF); ++q) prefetch_stage(q);
-            for (int q = 0; q < NQ; ++q) {
-                const int s = q & (NS - 1);
-                if (PF > 0 && q + NS + PF < NQ) prefetch_stage(q + NS + PF);
-                if (q >= NS) mbar_wait(empty + s, (uint32_t)(((q >> NSL) - 1) & 1));
-                const int64_t e = E0a + ((int64_t)q << CAP_LOG2);
-                const uint32_t cnt = (uint32_t)min((int64_t)CAP, E1a - e);
-                mbar_expect_tx(full + s, cnt * 12u);
-                bulk_g2s(scol + ((size_t)s << CAP_LOG2), a.col + e, cnt * 4u, full + s, pol);
-                bulk_g2s(sval + ((size_t)s << CAP_LOG2), a.val + e, cnt * 8u, full + s, pol);
+    auto chunk_rows = [&](int64_t c, int64_t* R0, int64_t* R1) {
+        *R0 = a.r_lo + ((c * K) << 5);
+        *R1 = min(*R0 + ((int64_t)K << 5), a.r_hi);
+    };
+
+    if (warp == W) {  // producer: each chunk's entry stream, stage by stage
+        if (lane != 0) return;
+        const uint64_t pol = evict_first_policy();
+        int q = 0;  // global stage number
+        int64_t c = blockIdx.x, R0, R1;
+        chunk_rows(c, &R0, &R1);
+        int64_t E0 = __ldg(a.rp + R0), E1 = __ldg(a.rp + R1);
+        while (true) {
+            const int64_t cn = c + gridDim.x;
+            int64_t E0n = 0, E1n = 0;
+            if (cn < n_chunks) {  // the next chunk's bounds, loaded under this chunk's copies
+                chunk_rows(cn, &R0, &R1);
+                E0n = __ldg(a.rp + R0);
+                E1n = __ldg(a.rp + R1);
             }
+            if (E1 > E0) {
+                const int64_t E0a = E0 & ~int64_t(3), E1a = (E1 + 3) & ~int64_t(3);
+                for (int64_t e = E0a; e < E1a; e += CAP, ++q) {
+                    const int s = q & (NS - 1);
+                    if (q >= NS) mbar_wait(empty + s, (uint32_t)(((q >> NSL) - 1) & 1));
+                    const uint32_t cnt = (uint32_t)min((int64_t)CAP, E1a - e);
+                    mbar_expect_tx(full + s, cnt * 12u);
+                    bulk_g2s(scol + ((size_t)s << CAP_LOG2), a.col + e, cnt * 4u, full + s, pol);
+                    bulk_g2s(sval + ((size_t)s << CAP_LOG2), a.val + e, cnt * 8u, full + s, pol);
+                }
+            }
+            if (cn >= n_chunks) break;
+            c = cn;
+            E0 = E0n;
+            E1 = E1n;
         }
         return;
     }
 
     const double sc = SCALE ? *a.x_scale : 1.0;
-    int passed = 0;  // stages [0, passed) waited for and released by this warp
-    int64_t g = g_lo + warp;
-    // this run's row pointers; the next run's are loaded while this one is summed
-    int kb = 0, ke = 0;
-    if (g < g_hi) {
-        const int64_t row = a.r_lo + (g << 5) + lane;
-        kb = __ldg(a.rp + min(row, R1));
-        ke = __ldg(a.rp + min(row + 1, R1));
-    }
-    for (; g < g_hi; g += W) {
-        const int64_t row = a.r_lo + (g << 5) + lane;
-        int kb_n = 0, ke_n = 0;
-        if (g + W < g_hi) {
-            const int64_t rn = row + ((int64_t)W << 5);
-            kb_n = __ldg(a.rp + min(rn, R1));
-            ke_n = __ldg(a.rp + min(rn + 1, R1));
+    int passed = 0;  // global stages [0, passed) waited for and released by this warp
+    int q_base = 0;  // global number of the current chunk's first stage
+    auto pass_to = [&](int q_end) {
+        for (; passed < q_end; ++passed) {
+            const int s = passed & (NS - 1);
+            mbar_wait(full + s, (uint32_t)((passed >> NSL) & 1));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
         }
-        const int ea = __shfl_sync(0xffffffffu, kb, 0), eb = __shfl_sync(0xffffffffu, ke, 31);
-        double acc = 0.0;
-        if (eb > ea) {
-            const int qa = (int)((ea - E0a) >> CAP_LOG2), qb = (int)((eb - 1 - E0a) >> CAP_LOG2);
-            for (; passed < qa; ++passed) {  // stages of the other warps' runs
-                const int s = passed & (NS - 1);
-                mbar_wait(full + s, (uint32_t)((passed >> NSL) & 1));
-                __syncwarp();
-                if (lane == 0) mbar_arrive(empty + s);
-            }
-            for (int q = qa; q <= qb; ++q) mbar_wait(full + (q & (NS - 1)), (uint32_t)((q >> NSL) & 1));
-            const int base = (int)E0a;
-            for (int p = kb; p < ke; p += UNROLL) {
-                int32_t c[UNROLL];
-                double v[UNROLL], xv[UNROLL];
-#pragma unroll
-                for (int j = 0; j < UNROLL; ++j) {
-                    const int i = (p + j - base) & mask;
-                    const bool ok = p + j < ke;
-                    c[j] = ok ? scol[i] : -1;
-                    v[j] = ok ? sval[i] : 0.0;
-                }
-#pragma unroll
-                for (int j = 0; j < UNROLL; ++j) xv[j] = c[j] >= 0 ? __ldg(a.x + ((int64_t)c[j] - a.row0)) : 0.0;
-#pragma unroll
-                for (int j = 0; j < UNROLL; ++j) {
-                    double t = xv[j];
-                    if (SCALE) t = __dmul_rn(t, sc);
-                    if (c[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], t));
-                }
-            }
+    };
+    for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+        int64_t R0, R1;
+        chunk_rows(c, &R0, &R1);
+        const int64_t g_lo = c * K, g_hi = min(g_lo + K, n_runs);
+        // the warp's first run of the chunk; lane 0 / 31 also fetch the chunk's bounds
+        int64_t g = g_lo + warp;
+        int kb = 0, ke = 0;
+        if (g < g_hi) {
+            const int64_t row = a.r_lo + (g << 5) + lane;
+            kb = __ldg(a.rp + min(row, R1));
+            ke = __ldg(a.rp + min(row + 1, R1));
         }
-        if (row < R1) a.y[row] = acc;
-        kb = kb_n;
-        ke = ke_n;
-    }
-    // let the producer finish the stream for the warps still at work
-    __syncwarp();
-    for (; passed < NQ; ++passed) {
-        const int s = (int)(passed & (NS - 1));
-        mbar_wait(full + s, (uint32_t)((passed >> NSL) & 1));
+        const int64_t E0 = __ldg(a.rp + R0), E1 = __ldg(a.rp + R1);
+        const int64_t E0a = E0 & ~int64_t(3);
+        const int NQ = E1 > E0 ? (int)((E1 - E0a + CAP - 1) >> CAP_LOG2) : 0;
+        // entry p of the chunk lives at ring slot (p - base) & mask (wrap-around arithmetic)
+        const uint32_t base = (uint32_t)E0a - ((uint32_t)q_base << CAP_LOG2);
+        for (; g < g_hi; g += W) {
+            const int64_t row = a.r_lo + (g << 5) + lane;
+            int kb_n = 0, ke_n = 0;
+            if (g + W < g_hi) {  // the next run's row pointers, loaded while this one is summed
+                const int64_t rn = row + ((int64_t)W << 5);
+                kb_n = __ldg(a.rp + min(rn, R1));
+                ke_n = __ldg(a.rp + min(rn + 1, R1));
+            }
+            const int ea = __shfl_sync(0xffffffffu, kb, 0), eb = __shfl_sync(0xffffffffu, ke, 31);
+            double acc = 0.0;
+            if (eb > ea) {
+                const int qa = q_base + (int)((ea - E0a) >> CAP_LOG2), qb = q_base + (int)((eb - 1 - E0a) >> CAP_LOG2);
+                pass_to(qa);  // stages of the other warps' runs
+                for (int q = qa; q <= qb; ++q) mbar_wait(full + (q & (NS - 1)), (uint32_t)((q >> NSL) & 1));
+                for (int p = kb; p < ke; p += UNROLL) {
+                    int32_t cc[UNROLL];
+                    double v[UNROLL], xv[UNROLL];
+#pragma unroll
+                    for (int j = 0; j < UNROLL; ++j) {
+                        const uint32_t i = ((uint32_t)(p + j) - base) & (uint32_t)mask;
+                        const bool ok = p + j < ke;
+                        cc[j] = ok ? scol[i] : -1;
+                        v[j] = ok ? sval[i] : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < UNROLL; ++j)
+                        xv[j] = cc[j] >= 0 ? __ldg(a.x + ((int64_t)cc[j] - a.row0)) : 0.0;
+#pragma unroll
+                    for (int j = 0; j < UNROLL; ++j) {
+                        double t = xv[j];
+                        if (SCALE) t = __dmul_rn(t, sc);
+                        if (cc[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], t));
+                    }
+                }
+            }
+            if (row < R1) a.y[row] = acc;
+            kb = kb_n;
+            ke = ke_n;
+        }
+        // the chunk's remaining stages: the producer can go on for the warps still at work
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
+        q_base += NQ;
+        pass_to(q_base);
     }
 }
 
@@ -229,7 +252,7 @@ bool rest_rows_launch(const Matrix& m, const double* x_local, double* y, const d
     const char* ew = getenv("HDCG_ROWS_W");  // read per call: the tests switch them in-process
     const char* es = getenv("HDCG_ROWS_STAGES");
     const int env_w = ew ? atoi(ew) : 0, env_ns = es ? atoi(es) : 0;
-    const char* ep = getenv("HDCG_ROWS_PF");
+    const char* ek = getenv("HDCG_ROWS_CHUNK");
     // runs of a launch start at r0, which need not be 32-aligned: a window of 32
     // rows overlaps at most two aligned runs
     const int64_t run_max = 2 * m.rest_run_max;
@@ -260,15 +283,14 @@ bool rest_rows_launch(const Matrix& m, const double* x_local, double* y, const d
     a.row0 = m.row0;
     a.r_lo = r0;
     a.r_hi = r1;
-    a.prefetch = ep ? atoi(ep) : 0;  // measured slower with any look-ahead (profiles/r02s_ab_rows.log)
+    a.chunk_runs = ek && atoi(ek) > 0 ? atoi(ek) : 4 * W;
     a.ns_log2 = 0;
     while ((1 << a.ns_log2) < NS) ++a.ns_log2;
     const size_t smem = (size_t)NS * CAP * 12 + sizeof(uint64_t) * 2 * NS;
     const int per_sm = std::max(1, std::min(2, (int)((227 * 1024) / (smem + 1024))));
     const int64_t n_runs = ceil_div(r1 - r0, 32);
-    // at least 4 runs per consumer warp and CTA: small row ranges take fewer CTAs
-    const int64_t want = std::max<int64_t>(1, n_runs / (4 * W));
-    const int grid = (int)std::min<int64_t>((int64_t)sm_count() * per_sm, want);
+    const int64_t n_chunks = ceil_div(n_runs, a.chunk_runs);
+    const int grid = (int)std::min<int64_t>((int64_t)sm_count() * per_sm, n_chunks);
     if (W == 16) {
         if (x_scale) launch_rows<16, true>(a, grid, smem, st);
         else launch_rows<16, false>(a, grid, smem, st);
