@@ -37,6 +37,13 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 GRID4 = (1024, 1024, 512)
+# Test hooks (tests/test_bench_gpu.py), never set by the driver: HDCG_BENCH_GRID=nx,ny,nz
+# shrinks config 4's grid and HDCG_BENCH_SHARED_GPU=1 puts every rank on cuda:0 with the
+# gloo backend, so the N > 1 code path of this file runs on a one-GPU box.  Either one
+# is reported in the JSON line ("test_mode"), which is then not a benchmark result.
+if os.environ.get("HDCG_BENCH_GRID"):
+    GRID4 = tuple(int(v) for v in os.environ["HDCG_BENCH_GRID"].split(","))
+SHARED_GPU = os.environ.get("HDCG_BENCH_SHARED_GPU") == "1"
 METRIC = "SpMV GFLOP/s (2*nnz)"
 UNIT = "GFLOP/s"
 THETA = 0.6
@@ -325,8 +332,12 @@ def run_ours(a):
     from paper_2105_04937_b200.dist import CudaSlab, SlabPlan, SlabRunner, all_ranks_agree
 
     rank, world, local = dist_env()
+    if SHARED_GPU:
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and SHARED_GPU:
+        dist.init_process_group("gloo")
+    elif world > 1:
         # NCCL on a high-priority stream: the halo send/recv kernel is dispatched ahead
         # of the interior SpMV's CTAs when both become ready after the boundary blocks
         opts = dist.ProcessGroupNCCL.Options()
@@ -349,7 +360,8 @@ def run_ours(a):
     use_p2p = False
     if world > 1 and a.halo != "nccl":
         nbrs = [j for j in (local - 1, local + 1) if 0 <= j < world]
-        use_p2p = all_ranks_agree(all(torch.cuda.can_device_access_peer(local, j) for j in nbrs), "cuda")
+        use_p2p = all_ranks_agree(SHARED_GPU or all(torch.cuda.can_device_access_peer(local, j) for j in nbrs),
+                                  "cuda")
     g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
     compute = CudaSlab(m, halo)
 
@@ -445,8 +457,8 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE config 4 generated on device; x uniform[-1,1] seed 5)",
-            "config": {"workload": "config4: 7-pt Laplacian 1024x1024x512, M-HDC bl=%d theta=0.6, "
-                                   "power iteration x<-y/||y||" % bl,
+            "config": {"workload": "config4: 7-pt Laplacian %dx%dx%d, M-HDC bl=%d theta=0.6, "
+                                   "power iteration x<-y/||y||" % (nx, ny, nz, bl),
                        "n": n, "nnz": nnz_total, "bl": bl, "theta": THETA,
                        "parallelism": f"row-slab x{world} (z-slabs), halo {halo} rows per neighbour"
                                       + {"p2p": ", stored by the boundary SpMV into the neighbours' buffers "
@@ -473,6 +485,8 @@ def run_ours(a):
         }
         if world > 1:
             result["halo_check"] = {"transport": halo_note, "ok_all_ranks": ok_all, **runner.halo_ok}
+        if SHARED_GPU or GRID4 != (1024, 1024, 512):
+            result["test_mode"] = {"grid": list(GRID4), "ranks_share_one_gpu_gloo": SHARED_GPU}
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
