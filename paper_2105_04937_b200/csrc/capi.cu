@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <cstdlib>
+
 #include "hdcg_internal.cuh"
 
 namespace hdcg {
@@ -260,6 +262,17 @@ hdcg_status hdcg_init(int device) {
         HDCG_CUDA(cudaSetDevice(device));
         check_arch(device);
         HDCG_CUDA(cudaFree(nullptr));
+        // HDCG_POOL_RETAIN_MB: freed device memory up to this size stays in the
+        // stream-ordered pool instead of going back to the driver at the next
+        // synchronisation (default: released) -- repeated conversions then skip
+        // the driver's page mapping, most of a large conversion's wall time
+        // (scripts/convert_bench.py measures both)
+        if (const char* e = getenv("HDCG_POOL_RETAIN_MB")) {
+            cudaMemPool_t pool;
+            HDCG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+            uint64_t keep = (uint64_t)atoll(e) << 20;
+            HDCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
     });
 }
 

@@ -27,6 +27,7 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "hdcg_internal.cuh"
@@ -141,19 +142,20 @@ template <class RP>
 __global__ void __launch_bounds__(CENSUS_THREADS)
 census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t row0, int64_t bl,
                      int64_t n_blocks, double theta, int32_t* sel_count, int32_t* stash,
-                     int32_t* blk_status, int32_t* ovf_list, int32_t* ovf_count) {
+                     int32_t* blk_status, int32_t* ovf_list, int32_t* ovf_count, int32_t* blk_rest) {
     __shared__ int32_t keys[HASH_CAP];
     __shared__ int32_t cnts[HASH_CAP];
     __shared__ int32_t sel[SEL_MAX];
     __shared__ int s_nsel;
     __shared__ int s_overflow;
+    __shared__ unsigned long long s_selected;  // entries on the selected offsets
     const int lane = threadIdx.x & 31;
     for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x) {
         for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x) {
             keys[s] = EMPTY_KEY;
             cnts[s] = 0;
         }
-        if (threadIdx.x == 0) { s_nsel = 0; s_overflow = 0; }
+        if (threadIdx.x == 0) { s_nsel = 0; s_overflow = 0; s_selected = 0; }
         __syncthreads();
         const int64_t r0 = b * bl, r1 = min(r0 + bl, n_rows), len = r1 - r0;
         volatile int* vovf = &s_overflow;
@@ -176,6 +178,7 @@ census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t 
                 if (k != EMPTY_KEY && (double)cnts[s] / (double)len >= theta) {
                     const int p = atomicAdd(&s_nsel, 1);
                     if (p < SEL_MAX) sel[p] = k;
+                    atomicAdd(&s_selected, (unsigned long long)cnts[s]);
                 }
             }
         }
@@ -195,9 +198,13 @@ census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t 
             if (threadIdx.x == 0) {
                 sel_count[b] = s_nsel;
                 blk_status[b] = 0;
+                // entries left for the remainder: 0 lets rest_count_kernel skip the block
+                const int64_t left = (rp[r1] - rp[r0]) - (int64_t)s_selected;
+                blk_rest[b] = (int32_t)min(left, (int64_t)INT32_MAX);
             }
         } else if (threadIdx.x == 0) {
             sel_count[b] = 0;
+            blk_rest[b] = -1;  // unknown: counted row by row
             blk_status[b] = -1;
             ovf_list[atomicAdd(ovf_count, 1)] = (int32_t)b;
         }
@@ -304,10 +311,16 @@ __global__ void write_offsets_kernel(int64_t n_blocks, const int32_t* dia_ptr, c
 template <class RP>
 __global__ void rest_count_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t row0,
                                   int64_t bl, const int32_t* dia_ptr, const int32_t* dia_off,
-                                  int32_t* rest_cnt) {
+                                  const int32_t* blk_rest, int32_t* rest_cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i / bl;
+        // every entry of the block lies on a selected offset (known from the census):
+        // no column is read
+        if (blk_rest && blk_rest[b] == 0) {
+            rest_cnt[i] = 0;
+            continue;
+        }
         const int32_t base = dia_ptr[b];
         const int32_t S = dia_ptr[b + 1] - base;
         const int32_t* sel = dia_off + base;
@@ -455,6 +468,7 @@ struct Selection {
     int32_t* dia_ptr = nullptr;  // [n_blocks+1]
     int32_t* dia_off = nullptr;  // [n_seg]
     int64_t n_seg = 0;
+    int32_t* blk_rest = nullptr;  // [n_blocks] unselected entries per block (-1 unknown), or null
 };
 
 // General-path machinery shared by to_mhdc (overflow blocks) and census export.
@@ -530,9 +544,10 @@ static Selection select_blocked(const CsrInput& in, double theta, int64_t bl, in
     int32_t* ovf_count = dev_alloc<int32_t>(1, st);
     HDCG_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int32_t), st));
     HDCG_CUDA(cudaMemsetAsync(sel_count + n_blocks, 0, sizeof(int32_t), st));
+    s.blk_rest = dev_alloc<int32_t>(n_blocks, st);
     census_select_kernel<RP><<<grid_cap(n_blocks), CENSUS_THREADS, 0, st>>>(
         rp, in.col, in.n_rows, in.row0, bl, n_blocks, theta, sel_count, stash, blk_status, ovf_list,
-        ovf_count);
+        ovf_count, s.blk_rest);
     HDCG_LAUNCH_CHECK("census_select_kernel");
     const int n_ovf = read_scalar(ovf_count, st);
     OvfRun<RP> ovf;
@@ -629,11 +644,15 @@ static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selec
     m->dia_off = sel.dia_off;
     int32_t* rest_cnt = dev_alloc<int32_t>(in.n_rows + 1, st);
     HDCG_CUDA(cudaMemsetAsync(rest_cnt + in.n_rows, 0, sizeof(int32_t), st));
+    // HDCG_CONVERT_SKIP=0: count every row's remainder from its columns (A/B knob)
+    const char* es = getenv("HDCG_CONVERT_SKIP");
+    const bool skip = !es || atoi(es) != 0;
     if (in.n_rows > 0) {
         rest_count_kernel<RP><<<grid_cap(ceil_div(in.n_rows, 256)), 256, 0, st>>>(
-            rp, in.col, in.n_rows, in.row0, bl, m->dia_ptr, m->dia_off, rest_cnt);
+            rp, in.col, in.n_rows, in.row0, bl, m->dia_ptr, m->dia_off, skip ? sel.blk_rest : nullptr, rest_cnt);
         HDCG_LAUNCH_CHECK("rest_count_kernel");
     }
+    dev_free(sel.blk_rest, st);
     const int64_t nnz_rest = in.nnz <= 0x7fffffffLL ? -1 : sum_i32_as_i64(rest_cnt, in.n_rows, st);
     if (nnz_rest > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "remainder nnz exceeds index range");
     m->rest_rp = dev_alloc<int32_t>(in.n_rows + 1, st);

@@ -535,6 +535,14 @@ def build_mhdc_device(n_rows, n_cols, row0, nnz, rp_ptr, col_ptr, val_ptr, theta
     return MHdcMatrix(h.value, theta)
 
 
+def build_hdc_device(n, nnz, rp_ptr, col_ptr, val_ptr, theta, rp64=True, validate=False, stream=0) -> "HdcMatrix":
+    """to_hdc from device-resident CSR arrays (the device twin of to_hdc)."""
+    h = _new_handle()
+    flags = HDCG_INPUT_DEVICE | (HDCG_ROWPTR_I64 if rp64 else 0) | (HDCG_VALIDATE if validate else 0)
+    check(lib().hdcg_build_hdc(n, nnz, rp_ptr, col_ptr, val_ptr, float(theta), flags, stream or None, C.byref(h)))
+    return HdcMatrix(h.value, theta)
+
+
 def gen_uniform_pm1(seed: int, rng_stream: int, first: int, count: int, out_ptr: int, stream=0):
     check(lib().hdcg_gen_uniform_pm1(seed, rng_stream, first, count, out_ptr, stream or None))
 
