@@ -76,6 +76,8 @@ typedef struct {
     int64_t device_bytes;
     int64_t max_seg_per_block; /* most segments in one block (selects the SpMV kernel) */
     int64_t packed_stages; /* >0: small blocks also stored tile-packed (1024-value stages) */
+    int64_t rest_rows_kernel; /* 1: remainder-first / CSR row sums take the row-per-lane kernel
+                                 (banded rows, sampled at build time), 0: the entry-major one */
 } hdcg_info;
 
 /* ---- runtime ------------------------------------------------------------ */

@@ -501,6 +501,7 @@ hdcg_status hdcg_get_info(hdcg_matrix h, hdcg_info* info) {
         info->device_bytes = m->device_bytes;
         info->max_seg_per_block = m->max_seg_per_block;
         info->packed_stages = m->packed ? m->pk_stages : 0;
+        info->rest_rows_kernel = rest_rows_default(*m) ? 1 : 0;
     });
 }
 

@@ -86,6 +86,7 @@ struct Matrix {
     int64_t n_seg = 0, nnz_rest = 0, nnz_input = 0, dia_slots = 0;
     int64_t max_seg_per_block = 0;  // selects rows per thread (tiling_of)
     int64_t rest_run_max = 0;       // most remainder entries in 32 aligned consecutive rows (rest_run_stats)
+    double rest_lines_per_gather = 32.0;  // distinct x lines per row-per-lane warp gather (sampled; rest_run_stats)
     int32_t* dia_ptr = nullptr;
     int32_t* dia_off = nullptr;
     double* seg = nullptr;
@@ -189,7 +190,8 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
 // false when the matrix is not eligible
 bool rest_rows_launch(const Matrix& m, const double* x_local, double* y, const double* x_scale, int64_t r0,
                       int64_t r1, cudaStream_t st);
-void rest_run_stats(Matrix* m);  // fills Matrix::rest_run_max (synchronous; after the build)
+bool rest_rows_default(const Matrix& m);  // the default policy picks rest_rows_kernel for this matrix
+void rest_run_stats(Matrix* m);  // fills Matrix::rest_run_max / rest_lines_per_gather (synchronous; after the build)
 extern int g_kernel_policy;  // 0 auto, 1 general kernel only, 2 TMA kernel only
 extern int g_rest_mode;      // TMA kernel remainder mode (hdcg_set_kernel_policy), 0 default
 // Matrix Market ingestion (mmio.cu)

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(32 * (W + 1), W >= 16 ? HDCG_ROWS_W16_CTAS : 2
     }
 
     const double sc = SCALE ? *a.x_scale : 1.0;
+    const double* __restrict__ xb = a.x - a.row0;  // x[c - row0] = xb[c]
     int passed = 0;  // global stages [0, passed) waited for and released by this warp
     int q_base = 0;  // global number of the current chunk's first stage
     auto pass_to = [&](int q_end) {
@@ -172,24 +173,43 @@ __global__ void __launch_bounds__(32 * (W + 1), W >= 16 ? HDCG_ROWS_W16_CTAS : 2
                 const int qa = q_base + (int)((ea - E0a) >> CAP_LOG2), qb = q_base + (int)((eb - 1 - E0a) >> CAP_LOG2);
                 pass_to(qa);  // stages of the other warps' runs
                 for (int q = qa; q <= qb; ++q) mbar_wait(full + (q & (NS - 1)), (uint32_t)((q >> NSL) & 1));
-                for (int p = kb; p < ke; p += UNROLL) {
-                    int32_t cc[UNROLL];
-                    double v[UNROLL], xv[UNROLL];
+                // The row's entries are contiguous in the ring unless they cross its end:
+                // the common case reads them at fixed offsets from one slot address
+                // (one LDS per column / value, no index arithmetic per entry).
+                const uint32_t i0 = ((uint32_t)kb - base) & (uint32_t)mask;
+                const int len = ke - kb;
+                if (i0 + (uint32_t)len <= (uint32_t)ring) {
+                    const int32_t* __restrict__ cp = scol + i0;
+                    const double* __restrict__ vp = sval + i0;
+                    int p = 0;
+                    for (; p + UNROLL <= len; p += UNROLL) {  // full batches: no predicates
+                        double xv[UNROLL];
 #pragma unroll
-                    for (int j = 0; j < UNROLL; ++j) {
-                        const uint32_t i = ((uint32_t)(p + j) - base) & (uint32_t)mask;
-                        const bool ok = p + j < ke;
-                        cc[j] = ok ? scol[i] : -1;
-                        v[j] = ok ? sval[i] : 0.0;
+                        for (int j = 0; j < UNROLL; ++j) xv[j] = __ldg(xb + cp[p + j]);
+#pragma unroll
+                        for (int j = 0; j < UNROLL; ++j) {
+                            double t = xv[j];
+                            if (SCALE) t = __dmul_rn(t, sc);
+                            acc = __dadd_rn(acc, __dmul_rn(vp[p + j], t));
+                        }
                     }
+                    if (p < len) {  // the last, partial batch
+                        double xv[UNROLL];
 #pragma unroll
-                    for (int j = 0; j < UNROLL; ++j)
-                        xv[j] = cc[j] >= 0 ? __ldg(a.x + ((int64_t)cc[j] - a.row0)) : 0.0;
+                        for (int j = 0; j < UNROLL; ++j) xv[j] = p + j < len ? __ldg(xb + cp[p + j]) : 0.0;
 #pragma unroll
-                    for (int j = 0; j < UNROLL; ++j) {
-                        double t = xv[j];
+                        for (int j = 0; j < UNROLL; ++j) {
+                            double t = xv[j];
+                            if (SCALE) t = __dmul_rn(t, sc);
+                            if (p + j < len) acc = __dadd_rn(acc, __dmul_rn(vp[p + j], t));
+                        }
+                    }
+                } else {  // the row wraps around the ring's end
+                    for (int p = 0; p < len; ++p) {
+                        const uint32_t i = (i0 + (uint32_t)p) & (uint32_t)mask;
+                        double t = __ldg(xb + scol[i]);
                         if (SCALE) t = __dmul_rn(t, sc);
-                        if (cc[j] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[j], t));
+                        acc = __dadd_rn(acc, __dmul_rn(sval[i], t));
                     }
                 }
             }
@@ -213,6 +233,39 @@ __global__ void run_max_kernel(const int32_t* __restrict__ rp, int64_t n_rows, i
     if ((threadIdx.x & 31) == 0 && mx > 0) atomicMax(out, mx);
 }
 
+// How well row-per-lane gathers coalesce: for every `stride`-th 32-row run, a warp
+// walks the rows like rest_rows_kernel does (lane = row, step k = the row's k-th
+// entry) and counts the distinct 128-byte x lines of each step's columns.
+// out[0] += lines, out[1] += steps.  Banded rows: 2-3 lines per step; random
+// columns: one line per lane.
+__global__ void run_lines_kernel(const int32_t* __restrict__ rp, const int32_t* __restrict__ col, int64_t n_rows,
+                                 int64_t stride, unsigned long long* out) {
+    const int64_t n_runs = (n_rows + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long lines = 0, steps = 0;
+    for (int64_t g = w * stride; g < n_runs; g += nw * stride) {
+        const int64_t row = (g << 5) + lane;
+        const int kb = row < n_rows ? rp[row] : 0, ke = row < n_rows ? rp[row + 1] : 0;
+        int len = ke - kb;
+        for (int o = 16; o; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+        len = min(len, 64);  // a long row's first entries tell enough
+        for (int k = 0; k < len; ++k) {
+            const bool ok = kb + k < ke;
+            const int line = ok ? (col[kb + k] >> 4) : -1 - lane;
+            const unsigned peers = __match_any_sync(0xffffffffu, line);
+            const unsigned leaders = __ballot_sync(0xffffffffu, ok && lane == __ffs(peers) - 1);
+            lines += __popc(leaders);
+            ++steps;
+        }
+    }
+    if (lane == 0 && steps) {
+        atomicAdd(out, lines);
+        atomicAdd(out + 1, steps);
+    }
+}
+
 template <int W, bool SCALE>
 void launch_rows(const RowsArgs& a, int grid, size_t smem, cudaStream_t st) {
     auto k = rest_rows_kernel<W, SCALE>;
@@ -228,16 +281,31 @@ void launch_rows(const RowsArgs& a, int grid, size_t smem, cudaStream_t st) {
 // once when the matrix is built: selects rest_rows_kernel (spmv_rows.cu).
 void rest_run_stats(Matrix* m) {
     m->rest_run_max = 0;
+    m->rest_lines_per_gather = 32.0;
     if (m->nnz_rest <= 0 || m->n_rows <= 0) return;
     DeviceGuard dg(m->device);
-    int* d = dev_alloc<int>(1, nullptr);
-    HDCG_CUDA(cudaMemsetAsync(d, 0, sizeof(int), nullptr));
-    run_max_kernel<<<grid_cap(ceil_div(ceil_div(m->n_rows, 32), 256)), 256>>>(m->rest_rp, m->n_rows, d);
+    unsigned long long* d = dev_alloc<unsigned long long>(3, nullptr);
+    HDCG_CUDA(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), nullptr));
+    const int64_t n_runs = ceil_div(m->n_rows, 32);
+    run_max_kernel<<<grid_cap(ceil_div(n_runs, 256)), 256>>>(m->rest_rp, m->n_rows, reinterpret_cast<int*>(d + 2));
     HDCG_LAUNCH_CHECK("run_max_kernel");
-    int v = 0;
-    HDCG_CUDA(cudaMemcpy(&v, d, sizeof(int), cudaMemcpyDeviceToHost));
+    const int64_t stride = std::max<int64_t>(1, n_runs / 4096);  // ~4096 sampled runs
+    run_lines_kernel<<<grid_cap(ceil_div(ceil_div(n_runs, stride), 8)), 256>>>(m->rest_rp, m->rest_col, m->n_rows,
+                                                                             stride, d);
+    HDCG_LAUNCH_CHECK("run_lines_kernel");
+    unsigned long long h[3] = {0, 0, 0};
+    HDCG_CUDA(cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost));
     dev_free(d, nullptr);
-    m->rest_run_max = v;
+    m->rest_run_max = (int64_t)(int)h[2];
+    if (h[1] > 0) m->rest_lines_per_gather = (double)h[0] / (double)h[1];
+}
+
+// The default policy's choice for a matrix (hdcg_info.rest_rows_kernel): banded rows
+// whose longest 32-row run fits the ring.
+bool rest_rows_default(const Matrix& m) {
+    if (m.nnz_rest <= 0 || m.rest_lines_per_gather > 8.0) return false;
+    if (((uintptr_t)m.rest_col % 16) != 0 || ((uintptr_t)m.rest_val % 16) != 0) return false;
+    return 2 * m.rest_run_max <= (int64_t)(16 - 1) * CAP;
 }
 
 // Remainder sums of local rows [r0, r1) into y (from +0.0).  False when the matrix
@@ -256,16 +324,20 @@ bool rest_rows_launch(const Matrix& m, const double* x_local, double* y, const d
     // runs of a launch start at r0, which need not be 32-aligned: a window of 32
     // rows overlaps at most two aligned runs
     const int64_t run_max = 2 * m.rest_run_max;
-    // Default: rows of >= 16 entries on average (a 27-point stencil as CSR: 864
-    // entries per run) take 16 warps and a 16-stage (192 KB) ring, one CTA per SM:
-    // config 2 as CSR 68% -> 81% of the HBM peak.  Short rows stay on
-    // rest_pipe_kernel, whose entry-major lanes keep more gathers in flight
-    // (config 1 as CSR 81% vs 79% here; config 3's random columns 61% vs 31%:
-    // profiles/r02s_ab_rows.log).  The knobs force this kernel (tests, A/B).
+    // Default: banded rows -- row-per-lane gathers of 32 adjacent rows touch few x
+    // lines (Matrix::rest_lines_per_gather, sampled at build time: 2-3 for a stencil
+    // stored as CSR, ~17 for config 3's rows with 6 random columns each) -- take this
+    // kernel with 16 warps; a 16-stage (192 KB) ring, one CTA per SM, when a 32-row
+    // run holds more than half a stage (27-point rows: 864 entries), else 8 stages
+    // and two CTAs per SM.  Configs 1 / 2 as CSR: 81% / 68% (rest_pipe_kernel) ->
+    // 92% / 94% of the HBM peak.  Rows with scattered columns stay on
+    // rest_pipe_kernel, whose entry-major lanes keep more gathers in flight (config
+    // 3 as CSR 61% vs 56% here; profiles/r02s_ab_rows.log).  The knobs force this
+    // kernel (tests, A/B).
     const int64_t avg_run = m.nnz_rest * 32 / std::max<int64_t>(1, m.n_rows);
-    if (!env_w && !env_ns && avg_run * 16 <= 8 * CAP) return false;
+    if (!env_w && !env_ns && m.rest_lines_per_gather > 8.0) return false;
     int W = env_w ? env_w : 16;
-    int NS = env_ns ? env_ns : 16;
+    int NS = env_ns ? env_ns : (avg_run * 16 > 8 * CAP ? 16 : 8);
     if (W != 8 && W != 16) return false;
     if (NS < 2 || (NS & (NS - 1)) || NS > 16) return false;
     if (run_max > (int64_t)(NS - 1) * CAP) {

@@ -81,7 +81,8 @@ class Info(C.Structure):
                 ("n_blocks", C.c_int64), ("n_seg", C.c_int64), ("nnz_rest", C.c_int64),
                 ("dia_slots", C.c_int64), ("nnz_input", C.c_int64), ("n_tiles", C.c_int64),
                 ("tile_rows", C.c_int64), ("blocks_per_tile", C.c_int64),
-                ("device_bytes", C.c_int64), ("max_seg_per_block", C.c_int64), ("packed_stages", C.c_int64)]
+                ("device_bytes", C.c_int64), ("max_seg_per_block", C.c_int64), ("packed_stages", C.c_int64),
+                ("rest_rows_kernel", C.c_int64)]
 
 
 _lib = None
@@ -576,11 +577,10 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
     if rest == 2 and info.n_seg > 0 and not blk and info.kind == KIND_MHDC:
         rest = 3  # gather warps inside the segment kernel
-    # remainder sums first: rows of >= 16 entries on average take the row-per-lane
-    # kernel with a TMA-staged entry ring (spmv_rows.cu) unless a 32-row run is
-    # longer than its ring, shorter rows the entry-major rest_pipe_kernel
-    long_rows = info.nnz_rest * 32 // max(1, info.n_rows) * 16 > 8 * 1024
-    ks = [("hdcg::rest_rows_kernel" if long_rows else "hdcg::rest_pipe_kernel")] if rest == 2 else []
+    # remainder sums first: banded rows take the row-per-lane kernel with a TMA-staged
+    # entry ring (spmv_rows.cu; info.rest_rows_kernel, decided from a sample of the
+    # rows at build time), scattered columns the entry-major rest_pipe_kernel
+    ks = [("hdcg::rest_rows_kernel" if info.rest_rows_kernel else "hdcg::rest_pipe_kernel")] if rest == 2 else []
     if rest == 2 and info.n_seg == 0 and not norm:
         return ks  # a CSR: the remainder kernel's sums are y
     if blk:

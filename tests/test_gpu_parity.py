@@ -294,6 +294,9 @@ def test_config1_full_size(port):
     refh = port.to_hdc(rp, col, val, 0.6)
     assert_mhdc_equal(h, refh)
     assert H.spmv_hdc(h, x).tobytes() == yc.tobytes()
+    dc = H.device_csr(A)  # banded rows: the row-per-lane remainder kernel (sampled at build time)
+    assert dc.info.rest_rows_kernel == 1
+    assert H.spmv_csr(A, x).tobytes() == yc.tobytes()
     for bl in (256, 1024, 4096, 16384):
         m = H.to_mhdc(A, 0.6, bl)
         ref = port.to_mhdc(rp, col, val, 0.6, bl)
@@ -351,6 +354,8 @@ def test_config3_quasi_diagonal(port):
     x = synth.x_vector(n, 4)
     A = csr(rp, col, val)
     yc = port.spmv_csr(rp, col, val, x, 0)
+    assert H.device_csr(A).info.rest_rows_kernel == 0  # 6 random columns per row: entry-major kernel
+    assert H.spmv_csr(A, x).tobytes() == yc.tobytes()
     for bl in (1024, 8192):
         m = H.to_mhdc(A, 0.6, bl)
         ref = port.to_mhdc(rp, col, val, 0.6, bl)
