@@ -6,7 +6,7 @@
 # Every output goes to gpurun_out/TAG/.  Steps run in order; a step's exit code
 # is appended to gpurun_out/TAG/status.txt and never stops the later steps.
 #   smoke                      __graft_entry__.smoke()
-#   tests[:EXPR]               pytest -m gpu (optionally -k EXPR)
+#   tests[:EXPR]               pytest -m gpu (optionally -k EXPR; "+" in EXPR stands for " or ")
 #   bw                         the box's HBM copy bandwidth (scripts/bw_probe.py)
 #   bench:NAME:ARGS            python bench.py ARGS (commas -> spaces) > NAME.json
 #   ref:NAME:ARGS              python bench.py --impl reference ARGS > NAME.json
@@ -26,7 +26,7 @@ for step in "$@"; do
   IFS=':' read -r kind a1 a2 a3 a4 a5 <<< "$step"
   case $kind in
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$O/smoke.log" 2>&1; st smoke $? ;;
-    tests) if [ -n "$a1" ]; then K=(-k "$a1"); else K=(); fi
+    tests) if [ -n "$a1" ]; then K=(-k "${a1//+/ or }"); else K=(); fi
            timeout 2400 python -m pytest tests -q -m gpu -rfE --durations=15 "${K[@]}" > "$O/pytest_gpu.log" 2>&1
            st tests $? ;;
     bw) timeout 120 python scripts/bw_probe.py > "$O/bw.json" 2>&1; st bw $? ;;

@@ -6,8 +6,9 @@ r of N launches per step (dist.SlabPowerIteration): the boundary blocks, the
 interior blocks, the local tile tree, the top tree over the rank roots and the
 scale copy -- with the two things that need a second GPU replaced by local
 stand-ins of the same size:
-  * "p2p":  the boundary SpMV's halo stores go to this rank's own halo regions
-            (local HBM stores instead of NVLink stores);
+  * "p2p1": dist.py's default -- one launch over every block whose epilogue stores the
+            halo rows, here into this rank's own halo regions (local HBM stores
+            instead of NVLink stores); "p2p": boundary blocks first, then the interior;
   * "nccl": the send/recv of 2 x H rows is a device-to-device copy of the same rows
             into the halo regions, issued on a side stream like NCCL's;
   * the all-gather of the rank roots is a copy of the local root into roots[r].
@@ -55,8 +56,12 @@ def run_rank(plan, rank, bl, mode, steps, warmup):
             red = c.tree(tiles)
             scale.copy_(red[1:2])
         else:
-            if mode == "p2p":
+            if mode == "p2p1":  # dist.py's default: one launch, the halo rows stored from its epilogue
                 lo = y.data_ptr() + 8 * (halo + rows) if has_lo else 0   # stands in for the neighbour's halo
+                hi = y.data_ptr() if has_hi else 0
+                c.spmv(x, y, 0, c.n_blocks, scale, tiles, lo, hi)
+            elif mode == "p2p":
+                lo = y.data_ptr() + 8 * (halo + rows) if has_lo else 0
                 hi = y.data_ptr() if has_hi else 0
                 for b0, b1 in parts:
                     c.spmv(x, y, b0, b1, scale, tiles, lo, hi)
@@ -73,9 +78,9 @@ def run_rank(plan, rank, bl, mode, steps, warmup):
                         y[halo + rows:].copy_(y[rows:rows + halo])
                     done = torch.cuda.Event()
                     done.record()
-            if interior[1] > interior[0]:
+            if mode != "p2p1" and interior[1] > interior[0]:
                 c.spmv(x, y, interior[0], interior[1], scale, tiles)
-            if mode != "p2p":
+            if mode == "nccl":
                 torch.cuda.current_stream().wait_event(done)
             local = c.tree(tiles)
             roots[rank:rank + 1].copy_(local[0:1])
@@ -118,7 +123,7 @@ def main():
     for world in [int(w) for w in a.worlds.split(",")]:
         plan = SlabPlan.make(n, a.bl, halo, world, unit=nx * ny)
         ranks = sorted({0, world // 2, world - 1})
-        for mode in (("none",) if world == 1 else ("p2p", "nccl")):
+        for mode in (("none",) if world == 1 else ("p2p1", "p2p", "nccl")):
             res = [run_rank(plan, r, a.bl, mode, a.steps, a.warmup) for r in ranks]
             worst = max(r["ms_per_step"] for r in res)
             if world == 1:
