@@ -23,10 +23,10 @@ The compute backend is injected: CudaSlab (libhdcgpu.so, the product) or, in
 the CPU tests only, an oracle-backed stand-in.  The halo transport is either
   * "nccl": torch.distributed send/recv of the boundary rows (NCCL over NVLink;
     gloo in the CPU tests), overlapped with the interior blocks, or
-  * "p2p": PeerHalo -- the boundary SpMV itself stores its halo rows into the
-    neighbours' buffers through peer memory (CUDA IPC mappings, NVLink P2P
-    stores from the kernel epilogue), so the exchange overlaps the computation
-    tile by tile and no collective is launched for it.  The per-step norm
+  * "p2p": PeerHalo -- the SpMV itself (one launch over every block) stores its halo
+    rows into the neighbours' buffers through peer memory (CUDA IPC mappings,
+    NVLink P2P stores from the kernel epilogue), so the exchange overlaps the
+    computation tile by tile and no collective is launched for it.  The per-step norm
     all-gather orders those stores before the neighbours' next reads (and
     their reads before the next overwrite: x/y are double-buffered).
 """
