@@ -27,6 +27,7 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -123,7 +124,13 @@ void validate_csr(const CsrInput& in, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // 1. shared-memory census + selection per block
 
-__device__ __forceinline__ bool hash_add(int32_t* keys, int32_t* cnts, int32_t off, int c) {
+// used / n_used: the slots that hold a key, in insertion order, while there are at
+// most USED_MAX of them -- a block with few distinct offsets (any stencil) is then
+// selected from and cleared through this list instead of the whole table, which
+// matters for small blocks (256 rows x 7 entries against 2048 slots).
+constexpr int USED_MAX = 128;
+__device__ __forceinline__ bool hash_add(int32_t* keys, int32_t* cnts, int32_t off, int c, int32_t* used,
+                                         int* n_used) {
     volatile int32_t* vkeys = keys;
     uint32_t h = ((uint32_t)off * 0x9E3779B1u) >> (32 - HASH_LOG2);
     for (int p = 0; p < HASH_MAX_PROBE; ++p) {
@@ -131,6 +138,10 @@ __device__ __forceinline__ bool hash_add(int32_t* keys, int32_t* cnts, int32_t o
         if (k == off) { atomicAdd(&cnts[h], c); return true; }
         if (k == EMPTY_KEY) {
             const int32_t prev = atomicCAS(&keys[h], EMPTY_KEY, off);
+            if (prev == EMPTY_KEY) {  // this thread claimed the slot
+                const int u = atomicAdd(n_used, 1);
+                if (u < USED_MAX) used[u] = (int32_t)h;
+            }
             if (prev == EMPTY_KEY || prev == off) { atomicAdd(&cnts[h], c); return true; }
         }
         h = (h + 1) & (HASH_CAP - 1);
@@ -149,13 +160,27 @@ census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t 
     __shared__ int s_nsel;
     __shared__ int s_overflow;
     __shared__ unsigned long long s_selected;  // entries on the selected offsets
+    __shared__ int32_t used[USED_MAX];
+    __shared__ int s_nused;
     const int lane = threadIdx.x & 31;
+    bool first = true;
     for (int64_t b = blockIdx.x; b < n_blocks; b += gridDim.x) {
-        for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x) {
-            keys[s] = EMPTY_KEY;
-            cnts[s] = 0;
+        // clear the table: only the slots the previous block used, when those are listed
+        const int prev_used = first ? USED_MAX + 1 : s_nused;
+        first = false;
+        if (prev_used <= USED_MAX) {
+            for (int s = threadIdx.x; s < prev_used; s += blockDim.x) {
+                keys[used[s]] = EMPTY_KEY;
+                cnts[used[s]] = 0;
+            }
+        } else {
+            for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x) {
+                keys[s] = EMPTY_KEY;
+                cnts[s] = 0;
+            }
         }
-        if (threadIdx.x == 0) { s_nsel = 0; s_overflow = 0; s_selected = 0; }
+        __syncthreads();  // prev_used was read by every thread before it is reset
+        if (threadIdx.x == 0) { s_nsel = 0; s_overflow = 0; s_selected = 0; s_nused = 0; }
         __syncthreads();
         const int64_t r0 = b * bl, r1 = min(r0 + bl, n_rows), len = r1 - r0;
         volatile int* vovf = &s_overflow;
@@ -167,13 +192,16 @@ census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t 
                 const int32_t off = (int32_t)((int64_t)col[k] - gi);
                 const unsigned peers = __match_any_sync(__activemask(), off);
                 if (lane == __ffs(peers) - 1) {
-                    if (!hash_add(keys, cnts, off, __popc(peers))) *vovf = 1;
+                    if (!hash_add(keys, cnts, off, __popc(peers), used, &s_nused)) *vovf = 1;
                 }
             }
         }
         __syncthreads();
         if (!s_overflow) {
-            for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x) {
+            const int nu = s_nused;
+            const int n_scan = nu <= USED_MAX ? nu : HASH_CAP;
+            for (int q = threadIdx.x; q < n_scan; q += blockDim.x) {
+                const int s = nu <= USED_MAX ? used[q] : q;
                 const int32_t k = keys[s];
                 if (k != EMPTY_KEY && (double)cnts[s] / (double)len >= theta) {
                     const int p = atomicAdd(&s_nsel, 1);
@@ -545,7 +573,9 @@ static Selection select_blocked(const CsrInput& in, double theta, int64_t bl, in
     HDCG_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int32_t), st));
     HDCG_CUDA(cudaMemsetAsync(sel_count + n_blocks, 0, sizeof(int32_t), st));
     s.blk_rest = dev_alloc<int32_t>(n_blocks, st);
-    census_select_kernel<RP><<<grid_cap(n_blocks), CENSUS_THREADS, 0, st>>>(
+    // one thread per row for blocks narrower than the CTA
+    const int threads = (int)std::min<int64_t>(CENSUS_THREADS, std::max<int64_t>(64, (bl + 31) / 32 * 32));
+    census_select_kernel<RP><<<grid_cap(n_blocks), threads, 0, st>>>(
         rp, in.col, in.n_rows, in.row0, bl, n_blocks, theta, sel_count, stash, blk_status, ovf_list,
         ovf_count, s.blk_rest);
     HDCG_LAUNCH_CHECK("census_select_kernel");
