@@ -92,9 +92,12 @@ __device__ __forceinline__ unsigned mix(unsigned a)
     a ^= a >> 16; a *= 0x7feb352dU; a ^= a >> 15; a *= 0x846ca68bU; a ^= a >> 16;
     return a;
 }
-template <int U>
+// FLAVOR: 0 ld.global.nc (__ldg), 1 ld.global.cg (L2 only), 2 texture fetch (int2 texels
+// of a linear texture over x), 3 ld.global.cv
+template <int U, int FLAVOR = 0>
 __global__ void __launch_bounds__(1024, 1)
-pure_kernel(const double* __restrict__ x, double* __restrict__ out, int iters, int K, int n, int wbits)
+pure_kernel(const double* __restrict__ x, double* __restrict__ out, int iters, int K, int n, int wbits,
+            cudaTextureObject_t tex = 0)
 {
     double acc = 0.0;
     const unsigned lane = threadIdx.x & 31, grp = lane / K;
@@ -108,7 +111,14 @@ pure_kernel(const double* __restrict__ x, double* __restrict__ out, int iters, i
             unsigned h = mix(((blockIdx.x * 1024u + (threadIdx.x & ~31u) + grp) * 131u + it) * 16u + u);
             unsigned line = (h & wmask) >> 4;
             unsigned within = mix(h + lane) & 15;
-            xv[u] = __ldg(x + base + line * 16 + within);
+            const long long idx = base + line * 16 + within;
+            if (FLAVOR == 0) xv[u] = __ldg(x + idx);
+            else if (FLAVOR == 1) xv[u] = __ldcg(x + idx);
+            else if (FLAVOR == 3) xv[u] = __ldcv(x + idx);
+            else {
+                const int2 t = tex1Dfetch<int2>(tex, (int)idx);
+                xv[u] = __hiloint2double(t.y, t.x);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) acc += xv[u];
@@ -121,6 +131,30 @@ extern "C" int gp_pure(const double* x, double* out, int iters, int K, int n, in
     if (u == 4) pure_kernel<4><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits);
     else if (u == 8) pure_kernel<8><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits);
     else if (u == 16) pure_kernel<16><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits);
+    else return -1;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int gp_pure_flavor(const double* x, double* out, int iters, int K, int n, int wbits, int flavor, int grid,
+                              void* stream)
+{
+    cudaStream_t s = (cudaStream_t)stream;
+    static cudaTextureObject_t tex = 0;
+    if (flavor == 2 && !tex) {
+        cudaResourceDesc rd = {};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = const_cast<double*>(x);
+        rd.res.linear.desc = cudaCreateChannelDesc<int2>();
+        rd.res.linear.sizeInBytes = (size_t)n * 8;
+        cudaTextureDesc td = {};
+        td.readMode = cudaReadModeElementType;
+        cudaError_t e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+        if (e != cudaSuccess) return (int)e;
+    }
+    if (flavor == 0) pure_kernel<8, 0><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits);
+    else if (flavor == 1) pure_kernel<8, 1><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits);
+    else if (flavor == 2) pure_kernel<8, 2><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits, tex);
+    else if (flavor == 3) pure_kernel<8, 3><<<grid, 1024, 0, s>>>(x, out, iters, K, n, wbits);
     else return -1;
     return (int)cudaGetLastError();
 }

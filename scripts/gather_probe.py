@@ -17,6 +17,7 @@ L = ctypes.CDLL(os.path.join(HERE, "libgather_probe.so"))
 P = ctypes.c_void_p
 L.gp_probe.argtypes = [P, P, P, P, P] + [ctypes.c_int] * 8 + [P]
 L.gp_pure.argtypes = [P, P] + [ctypes.c_int] * 6 + [P]
+L.gp_pure_flavor.argtypes = [P, P] + [ctypes.c_int] * 6 + [P]
 L.gp_dsmem.argtypes = [P, P] + [ctypes.c_int] * 5 + [P]
 dev = torch.device("cuda")
 n = 1 << 24
@@ -104,8 +105,23 @@ def pure(K, u, grid, wbits=17):
                       "sector_gbs_if_1_per_load": round(loads * 32 / (ms * 1e-3) / 1e9, 1)}), flush=True)
 
 
+def flavor(f, K, grid=296, wbits=17):
+    iters = 256
+    out = torch.zeros(grid * 1024, dtype=torch.float64, device=dev)
+    fn = lambda: L.gp_pure_flavor(x.data_ptr(), out.data_ptr(), iters, K, n, wbits, f, grid, stream)
+    ms = timed(fn)
+    loads = grid * 1024 * 8 * iters
+    print(json.dumps({"pure_gather_flavor": ["ld.global.nc", "ld.global.cg", "tex1Dfetch<int2>", "ld.global.cv"][f],
+                      "lanes_per_line": K, "grid": grid, "ms": round(ms, 4), "checksum": float(out.sum().item()),
+                      "loads_per_cycle_sm": round(loads / (ms * 1e-3) / 1.965e9 / 148, 3)}), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["pure", "l2", "streams", "dsmem"]
+    if "flavor" in which:    # does another load path beat the 1-lookup-per-cycle L1 front end?
+        for K in (1, 4):
+            for f in (0, 1, 3, 2):
+                flavor(f, K)
     if "pure" in which:      # the chip's random-gather rate: no index streams
         for K in (1, 2, 4, 8):
             for u in (4, 8, 16):
