@@ -1249,7 +1249,13 @@ bool spmv_tma_launch(const Matrix& m, const double* x_local, double* y, int64_t 
     // Mode 3 is the default for remainder-heavy M-HDC (config 3: 0.62-0.65 ms
     // against 0.68 ms for mode 2, profiles/r02i_ab_fused_smem_sweep.log); HDC
     // (one block of n rows) measured 3% slower fused than split, so it keeps mode 2.
-    int mode = req >= 1 && req <= 3 ? req : (heavy ? (fusable && m.kind == HDCG_KIND_MHDC ? 3 : 2) : 1);
+    // A banded heavy remainder (a stencil converted with a high theta: rows of
+    // adjacent columns) is summed first by rest_rows_kernel, which runs near the HBM
+    // peak there (27-point 192^3 at theta = 1: 0.39 ms split vs 0.57 ms fused,
+    // profiles/r03k_ab_theta1.log); the gather warps are for scattered columns.
+    const bool banded = rest_rows_default(m);
+    int mode = req >= 1 && req <= 3 ? req
+                                    : (heavy ? (fusable && m.kind == HDCG_KIND_MHDC && !banded ? 3 : 2) : 1);
     if (mode == 3 && !fusable) mode = 2;
     const bool split = a.has_rest && mode == 2;
     a.fused = a.has_rest && mode == 3;

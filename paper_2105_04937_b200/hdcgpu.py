@@ -568,6 +568,8 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     b = lambda v: str(v).lower()  # noqa: E731
     if info.packed_stages > 0:  # tile-packed small blocks (pack.cu)
         rest = 0 if info.nnz_rest == 0 else (3 if info.nnz_rest * 4 >= info.n_rows else 1)
+        if rest == 3 and info.rest_rows_kernel:  # banded heavy remainder: summed first (spmv_rows.cu)
+            return ["hdcg::rest_rows_kernel", f"hdcg::spmv_tma_kernel<4,{b(scale)},{b(norm)},2,5>"]
         return [f"hdcg::spmv_tma_kernel<4,{b(scale)},{b(norm)},{rest},5>"]
     inside = info.bl >= info.tile_rows  # tiles inside one block, else whole blocks per tile
     mb = not inside and r == 4 and info.bl % 128 == 0
@@ -575,8 +577,8 @@ def spmv_kernels(info: Info, scale: bool = False, norm: bool = False) -> list:
     if not ((info.bl >= 256 and inside) or mb or blk):
         return [f"hdcg::spmv_kernel<{r},{b(scale)},{b(norm)}>"]
     rest = 0 if info.nnz_rest == 0 else (2 if info.nnz_rest * 4 >= info.n_rows else 1)
-    if rest == 2 and info.n_seg > 0 and not blk and info.kind == KIND_MHDC:
-        rest = 3  # gather warps inside the segment kernel
+    if rest == 2 and info.n_seg > 0 and not blk and info.kind == KIND_MHDC and not info.rest_rows_kernel:
+        rest = 3  # gather warps inside the segment kernel (scattered columns)
     # remainder sums first: banded rows take the row-per-lane kernel with a TMA-staged
     # entry ring (spmv_rows.cu; info.rest_rows_kernel, decided from a sample of the
     # rows at build time), scattered columns the entry-major rest_pipe_kernel

@@ -20,6 +20,9 @@ from paper_2105_04937_b200 import hdcgpu as H  # noqa: E402
 from paper_2105_04937_b200 import synth  # noqa: E402
 
 
+THETA = float(os.environ.get("HDCG_AB_THETA", "0.6"))  # fill threshold of the conversions (A/B knob)
+
+
 def matrix(w):
     path = f"/tmp/hdcg_ab_{w}.npz"
     if os.path.exists(path):
@@ -49,9 +52,9 @@ def main():
         if fmt == "csr":
             m = H.device_csr(A)
         elif fmt == "hdc":
-            m = H.to_hdc(A, 0.6, validate=False)
+            m = H.to_hdc(A, THETA, validate=False)
         else:
-            m = H.to_mhdc(A, 0.6, int(fmt), validate=False)
+            m = H.to_mhdc(A, THETA, int(fmt), validate=False)
         info = m.info
         x = torch.from_numpy(synth.x_vector(n, seed)).cuda()
         y = torch.empty(n, dtype=torch.float64, device="cuda")
