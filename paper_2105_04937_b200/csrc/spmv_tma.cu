@@ -423,6 +423,22 @@ __device__ __forceinline__ void gather_rest_rows(const TmaArgs& a, int64_t w0, i
 // sums of whole tiles ahead into y, up to RS_SLOTS tiles in flight); the
 // consumers start each row from its sum.  One CTA per SM: the x gathers need
 // about as many warps in flight as rest_pipe_kernel has (24 per SM).
+// Tile order of a persistent CTA.  HDCG_TILE_GROUP = 1 (default): tiles c, c + grid,
+// ...; G > 1 (A/B builds): G adjacent tiles in a row, then the next group -- the x
+// lines one tile loads for its +tile_rows offsets are the next tile's own rows.
+// Measured slower: config 4 1292 -> 1244 (G = 2) / 1242 (G = 4) GFLOP/s, configs 1-2
+// unchanged (profiles/r03o_ab_tile_group.log); the interleaved order stays.
+#ifndef HDCG_TILE_GROUP
+#define HDCG_TILE_GROUP 1
+#endif
+__device__ __forceinline__ int first_tile(const TmaArgs& a) { return a.tile_begin + HDCG_TILE_GROUP * (int)blockIdx.x; }
+__device__ __forceinline__ int next_tile(const TmaArgs& a, int tile) {
+    if (HDCG_TILE_GROUP == 1) return tile + (int)gridDim.x;
+    return (tile - a.tile_begin) % HDCG_TILE_GROUP != HDCG_TILE_GROUP - 1
+               ? tile + 1
+               : tile + HDCG_TILE_GROUP * (int)gridDim.x - (HDCG_TILE_GROUP - 1);
+}
+
 template <int R, bool SCALE, bool NORM, int REST, int LAY>
 __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THREADS, REST == 3 ? 1 : 3)
     spmv_tma_kernel(const TmaArgs a) {
@@ -468,7 +484,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
             int32_t* rps = S.grp + gw * (GCHUNK + 1);
             const double sc = SCALE ? *a.x_scale : 1.0;
             int k = 0;  // index among this CTA's non-empty tiles (the consumers count the same)
-            for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
+            for (int tile = first_tile(a); tile < a.tile_end; tile = next_tile(a, tile)) {
                 const Geo g = geo<R, MB, PK>(a, tile);
                 if (g.lo >= g.hi) continue;  // the consumers skip it too
                 const int kk = k++;
@@ -494,7 +510,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         int ps = 0;              // ring stage the next slice goes to
         uint32_t pphase = 0;     // parity of that stage's current use
         bool p_wrapped = false;  // every stage has been used once
-        for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
+        for (int tile = first_tile(a); tile < a.tile_end; tile = next_tile(a, tile)) {
             const Geo g = geo<R, MB, PK>(a, tile);
             if (g.lo >= g.hi) continue;
             if (a.prefetch && lane == 0) {
@@ -610,12 +626,12 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
         pe0 = __ldg(a.rest_rp + q.lo);
         pe1 = __ldg(a.rest_rp + q.hi);
     };
-    probe(a.tile_begin + blockIdx.x);
-    for (int tile = a.tile_begin + blockIdx.x; tile < a.tile_end; tile += gridDim.x) {
+    probe(first_tile(a));
+    for (int tile = first_tile(a); tile < a.tile_end; tile = next_tile(a, tile)) {
         const Geo g = geo<R, MB, PK>(a, tile);
         if (g.lo >= g.hi) {
             if (NORM && threadIdx.x == 0) a.tile_sumsq[tile] = 0.0;
-            probe(tile + gridDim.x);
+            probe(next_tile(a, tile));
             continue;
         }
         const int rows = (int)(g.hi - g.lo);
@@ -644,7 +660,7 @@ __global__ void __launch_bounds__(REST == 3 ? THREADS + 32 * GATHER_WARPS : THRE
             // a light remainder: most tiles have no entries.  The tile's entry range
             // was loaded one tile ahead, so those tiles issue no dependent load here.
             const bool any = pe0 < pe1;
-            probe(tile + gridDim.x);
+            probe(next_tile(a, tile));
             if (any) {
                 if constexpr (!MB) {  // the warp's rows are R runs of 32
 #pragma unroll
