@@ -228,9 +228,11 @@ class SlabPowerIteration:
         self.p2p_single_launch = True  # False: boundary blocks first, then the interior (A/B)
         self.yi = 1  # index (into the original pair) of the buffer y goes to this step
         dev = x0_buf.device
-        self.scale = torch.ones(1, dtype=torch.float64, device=dev)
+        # red = [sum of squares, 1/sqrt(sum)]; the scale the next SpMV applies is red[1],
+        # written in place by the top tree (no copy kernel between the steps)
+        self.red = torch.tensor([0.0, 1.0], dtype=torch.float64, device=dev)
+        self.scale = self.red[1:2]
         self.tiles = torch.zeros(compute.n_tiles, dtype=torch.float64, device=dev)
-        self.red = torch.zeros(2, dtype=torch.float64, device=dev)
         self.roots = torch.zeros(plan.world, dtype=torch.float64, device=dev)
         self.halo = HaloExchange(plan, rank)
         self.comm = comm and plan.world > 1
@@ -242,13 +244,20 @@ class SlabPowerIteration:
                 torch.cuda.synchronize(dev)
             dist.barrier()
 
+    def _top_tree(self, vals):
+        """The pairwise tree over `vals` (tile partials, or the rank roots) into
+        self.red; red[1] is the next step's scale."""
+        into = getattr(self.c, "tree_into", None)
+        if into is not None:
+            into(vals, self.red)
+        else:  # backends with tree() only (the CPU stand-in of the tests)
+            self.red.copy_(self.c.tree(vals))
+
     def step(self):
         x, y = self.bufs
         if not self.comm:
             self.c.spmv(x, y, 0, self.c.n_blocks, self.scale, self.tiles)
-            red = self.c.tree(self.tiles)
-            self.scale.copy_(red[1:2])
-            self.red = red
+            self._top_tree(self.tiles)
         elif self.peer is not None:
             # boundary blocks store their halo rows straight into the neighbours' y
             # buffers (same parity on every rank); the all-gather below orders them
@@ -266,8 +275,7 @@ class SlabPowerIteration:
                     self.c.spmv(x, y, self.interior[0], self.interior[1], self.scale, self.tiles)
             local = self.c.tree(self.tiles)
             _all_gather_roots(self.roots, local[0:1].contiguous())
-            self.red = self.c.tree(self.roots)
-            self.scale.copy_(self.red[1:2])
+            self._top_tree(self.roots)
         else:
             for b0, b1 in self.parts:
                 self.c.spmv(x, y, b0, b1, self.scale, self.tiles)
@@ -279,8 +287,7 @@ class SlabPowerIteration:
             _all_gather_roots(self.roots, local[0:1].contiguous())
             # the top of the tree over the rank roots: the same padded pairwise tree,
             # one launch on the device (stream-ordered after the all-gather)
-            self.red = self.c.tree(self.roots)
-            self.scale.copy_(self.red[1:2])
+            self._top_tree(self.roots)
         self.bufs.reverse()
         self.yi ^= 1
         return self.red
@@ -438,7 +445,11 @@ class CudaSlab:
     def tree(self, tiles):
         if self._out is None:
             self._out = torch.empty(2, dtype=torch.float64, device=tiles.device)
+        return self.tree_into(tiles, self._out)
+
+    def tree_into(self, tiles, out):
+        """out[0] = the pairwise-tree sum of `tiles`, out[1] = 1/sqrt(out[0])."""
         st = torch.cuda.current_stream().cuda_stream
-        self.H.tree_sum(tiles.data_ptr(), tiles.numel(), self._out.data_ptr(), st)
+        self.H.tree_sum(tiles.data_ptr(), tiles.numel(), out.data_ptr(), st)
         self.launches += 1 if tiles.numel() <= 2048 else 2
-        return self._out
+        return out

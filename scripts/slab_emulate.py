@@ -3,8 +3,7 @@
 Only one GPU is available to this build, so the N > 1 step cannot be timed over
 NVLink here.  This script runs, in one process, exactly the kernel sequence rank
 r of N launches per step (dist.SlabPowerIteration): the boundary blocks, the
-interior blocks, the local tile tree, the top tree over the rank roots and the
-scale copy -- with the two things that need a second GPU replaced by local
+interior blocks, the local tile tree and the top tree over the rank roots -- with the two things that need a second GPU replaced by local
 stand-ins of the same size:
   * "p2p1": dist.py's default -- one launch over every block whose epilogue stores the
             halo rows, here into this rank's own halo regions (local HBM stores
@@ -42,7 +41,8 @@ def run_rank(plan, rank, bl, mode, steps, warmup):
     bufs = [torch.zeros(rows + 2 * halo, dtype=torch.float64, device="cuda") for _ in range(2)]
     g0, g1 = max(0, row0 - halo), min(n, row0 + rows + halo)
     H.gen_uniform_pm1(5, 0, g0, g1 - g0, bufs[0].data_ptr() + 8 * (g0 - (row0 - halo)))
-    scale = torch.ones(1, dtype=torch.float64, device="cuda")
+    red = torch.tensor([0.0, 1.0], dtype=torch.float64, device="cuda")
+    scale = red[1:2]  # the top tree writes the next step's scale in place (dist.SlabPowerIteration)
     tiles = torch.zeros(c.n_tiles, dtype=torch.float64, device="cuda")
     roots = torch.zeros(plan.world, dtype=torch.float64, device="cuda")
     parts, interior = plan.boundary_blocks(rank, c.blocks_per_tile)
@@ -53,8 +53,7 @@ def run_rank(plan, rank, bl, mode, steps, warmup):
         x, y = bufs
         if plan.world == 1:
             c.spmv(x, y, 0, c.n_blocks, scale, tiles)
-            red = c.tree(tiles)
-            scale.copy_(red[1:2])
+            c.tree_into(tiles, red)
         else:
             if mode == "p2p1":  # dist.py's default: one launch, the halo rows stored from its epilogue
                 lo = y.data_ptr() + 8 * (halo + rows) if has_lo else 0   # stands in for the neighbour's halo
@@ -84,8 +83,7 @@ def run_rank(plan, rank, bl, mode, steps, warmup):
                 torch.cuda.current_stream().wait_event(done)
             local = c.tree(tiles)
             roots[rank:rank + 1].copy_(local[0:1])
-            red = c.tree(roots)
-            scale.copy_(red[1:2])
+            c.tree_into(roots, red)
         bufs.reverse()
 
     for _ in range(warmup):
