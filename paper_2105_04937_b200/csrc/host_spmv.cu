@@ -21,14 +21,16 @@ namespace hdcg {
 
 namespace {
 
-// Pipeline granularity: pieces of ~32 MB of x (at least 32, at most 256 chunks),
+// Pipeline granularity: pieces of ~32 MB of x (at least 16, at most 256 chunks),
 // so the fill (the first chunk's x) and the drain (the last chunk's y) stay a
-// small part of the PCIe time.  HDCG_PIPE_CHUNKS overrides (A/B).
+// small part of the PCIe time.  Each chunk costs ~20 us of launches and event
+// waits: 16 chunks beat 32 on the 134 MB vectors of configs 1 and 3 (3.40 vs
+// 3.65 ms per call) and on config 2 (1.75 vs 1.94 ms).  HDCG_PIPE_CHUNKS overrides (A/B).
 int pipe_chunks(int64_t n_cols) {
     static const int env = getenv("HDCG_PIPE_CHUNKS") ? atoi(getenv("HDCG_PIPE_CHUNKS")) : 0;
     if (env > 0) return env;
     const int64_t want = ceil_div(8 * n_cols, (int64_t)32 << 20);
-    return (int)std::min<int64_t>(256, std::max<int64_t>(32, want));
+    return (int)std::min<int64_t>(256, std::max<int64_t>(16, want));
 }
 
 // per tile: highest global column any of its rows reads (-1: none)
