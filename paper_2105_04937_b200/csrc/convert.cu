@@ -28,6 +28,8 @@
 #include <thrust/iterator/transform_iterator.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -41,6 +43,27 @@ constexpr int HASH_CAP = 1 << HASH_LOG2;
 constexpr int HASH_MAX_PROBE = 64;
 constexpr int SEL_MAX = 32;
 constexpr int32_t EMPTY_KEY = INT32_MIN;
+
+// HDCG_TRACE_BUILD=1: wall time of each conversion stage on stderr (each mark
+// synchronises the stream: a diagnostic, not for timed runs)
+struct BuildTrace {
+    bool on;
+    cudaStream_t st;
+    std::chrono::steady_clock::time_point t0;
+    explicit BuildTrace(cudaStream_t s) : on(getenv("HDCG_TRACE_BUILD") != nullptr), st(s) {
+        if (on) {
+            cudaStreamSynchronize(st);
+            t0 = std::chrono::steady_clock::now();
+        }
+    }
+    void mark(const char* what) {
+        if (!on) return;
+        cudaStreamSynchronize(st);
+        const auto t1 = std::chrono::steady_clock::now();
+        fprintf(stderr, "[hdcg build] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    }
+};
 
 template <class RP>
 struct RowPtr {
@@ -229,9 +252,11 @@ census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t 
                 // entries left for the remainder: 0 lets rest_count_kernel skip the block
                 const int64_t left = (rp[r1] - rp[r0]) - (int64_t)s_selected;
                 blk_rest[b] = (int32_t)min(left, (int64_t)INT32_MAX);
+                if (left != 0) ovf_count[1] = 1;  // the matrix has a remainder (benign race: every writer stores 1)
             }
         } else if (threadIdx.x == 0) {
             sel_count[b] = 0;
+            ovf_count[1] = 1;
             blk_rest[b] = -1;  // unknown: counted row by row
             blk_status[b] = -1;
             ovf_list[atomicAdd(ovf_count, 1)] = (int32_t)b;
@@ -497,6 +522,7 @@ struct Selection {
     int32_t* dia_off = nullptr;  // [n_seg]
     int64_t n_seg = 0;
     int32_t* blk_rest = nullptr;  // [n_blocks] unselected entries per block (-1 unknown), or null
+    bool no_rest = false;         // the census found every entry on a selected offset
 };
 
 // General-path machinery shared by to_mhdc (overflow blocks) and census export.
@@ -564,13 +590,14 @@ template <class RP>
 static Selection select_blocked(const CsrInput& in, double theta, int64_t bl, int64_t n_blocks,
                                 cudaStream_t st) {
     Selection s;
+    BuildTrace tr(st);
     RowPtr<RP> rp{(const RP*)in.row_ptr};
     int32_t* sel_count = dev_alloc<int32_t>(n_blocks + 1, st);
     int32_t* stash = dev_alloc<int32_t>(n_blocks * SEL_MAX, st);
     int32_t* blk_status = dev_alloc<int32_t>(n_blocks, st);
     int32_t* ovf_list = dev_alloc<int32_t>(n_blocks, st);
-    int32_t* ovf_count = dev_alloc<int32_t>(1, st);
-    HDCG_CUDA(cudaMemsetAsync(ovf_count, 0, sizeof(int32_t), st));
+    int32_t* ovf_count = dev_alloc<int32_t>(2, st);  // [overflowed blocks, any block with a remainder]
+    HDCG_CUDA(cudaMemsetAsync(ovf_count, 0, 2 * sizeof(int32_t), st));
     HDCG_CUDA(cudaMemsetAsync(sel_count + n_blocks, 0, sizeof(int32_t), st));
     s.blk_rest = dev_alloc<int32_t>(n_blocks, st);
     // one thread per row for blocks narrower than the CTA
@@ -579,7 +606,12 @@ static Selection select_blocked(const CsrInput& in, double theta, int64_t bl, in
         rp, in.col, in.n_rows, in.row0, bl, n_blocks, theta, sel_count, stash, blk_status, ovf_list,
         ovf_count, s.blk_rest);
     HDCG_LAUNCH_CHECK("census_select_kernel");
-    const int n_ovf = read_scalar(ovf_count, st);
+    int32_t flags[2] = {0, 0};
+    HDCG_CUDA(cudaMemcpyAsync(flags, ovf_count, sizeof(flags), cudaMemcpyDeviceToHost, st));
+    HDCG_CUDA(cudaStreamSynchronize(st));
+    const int n_ovf = flags[0];
+    s.no_rest = flags[1] == 0;
+    tr.mark("census + select");
     OvfRun<RP> ovf;
     if (n_ovf > 0) {
         // deterministic order of the irregular blocks
@@ -608,6 +640,7 @@ static Selection select_blocked(const CsrInput& in, double theta, int64_t bl, in
                                                                 ovf.out, ovf.start, s.dia_off);
         HDCG_LAUNCH_CHECK("write_offsets_kernel");
     }
+    tr.mark("overflow blocks, offsets");
     ovf.release(st);
     dev_free(sel_count, st);
     dev_free(stash, st);
@@ -663,6 +696,7 @@ template <class RP>
 static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selection sel, Matrix* m,
                          cudaStream_t st) {
     RowPtr<RP> rp{(const RP*)in.row_ptr};
+    BuildTrace tr(st);
     m->n_rows = in.n_rows;
     m->n_cols = in.n_cols;
     m->row0 = in.row0;
@@ -672,27 +706,35 @@ static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selec
     m->nnz_input = in.nnz;
     m->dia_ptr = sel.dia_ptr;
     m->dia_off = sel.dia_off;
-    int32_t* rest_cnt = dev_alloc<int32_t>(in.n_rows + 1, st);
-    HDCG_CUDA(cudaMemsetAsync(rest_cnt + in.n_rows, 0, sizeof(int32_t), st));
+    // remainder row pointers: per-row counts written into rest_rp and scanned in place
+    // (no second n-row array); a matrix whose census left nothing for the remainder
+    // (every stencil configuration) just gets zeros
+    m->rest_rp = dev_alloc<int32_t>(in.n_rows + 1, st);
     // HDCG_CONVERT_SKIP=0: count every row's remainder from its columns (A/B knob)
     const char* es = getenv("HDCG_CONVERT_SKIP");
     const bool skip = !es || atoi(es) != 0;
-    if (in.n_rows > 0) {
-        rest_count_kernel<RP><<<grid_cap(ceil_div(in.n_rows, 256)), 256, 0, st>>>(
-            rp, in.col, in.n_rows, in.row0, bl, m->dia_ptr, m->dia_off, skip ? sel.blk_rest : nullptr, rest_cnt);
-        HDCG_LAUNCH_CHECK("rest_count_kernel");
+    if (skip && sel.no_rest) {
+        HDCG_CUDA(cudaMemsetAsync(m->rest_rp, 0, sizeof(int32_t) * (in.n_rows + 1), st));
+    } else {
+        int32_t* rest_cnt = m->rest_rp;
+        HDCG_CUDA(cudaMemsetAsync(rest_cnt + in.n_rows, 0, sizeof(int32_t), st));
+        if (in.n_rows > 0) {
+            rest_count_kernel<RP><<<grid_cap(ceil_div(in.n_rows, 256)), 256, 0, st>>>(
+                rp, in.col, in.n_rows, in.row0, bl, m->dia_ptr, m->dia_off, skip ? sel.blk_rest : nullptr, rest_cnt);
+            HDCG_LAUNCH_CHECK("rest_count_kernel");
+        }
+        const int64_t nnz_rest = in.nnz <= 0x7fffffffLL ? -1 : sum_i32_as_i64(rest_cnt, in.n_rows, st);
+        if (nnz_rest > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "remainder nnz exceeds index range");
+        exclusive_scan(rest_cnt, m->rest_rp, in.n_rows + 1, st);  // in place
     }
     dev_free(sel.blk_rest, st);
-    const int64_t nnz_rest = in.nnz <= 0x7fffffffLL ? -1 : sum_i32_as_i64(rest_cnt, in.n_rows, st);
-    if (nnz_rest > 0x7fffffffLL) fail(HDCG_ERR_OVERFLOW, "remainder nnz exceeds index range");
-    m->rest_rp = dev_alloc<int32_t>(in.n_rows + 1, st);
-    exclusive_scan(rest_cnt, m->rest_rp, in.n_rows + 1, st);
-    dev_free(rest_cnt, st);
     m->nnz_rest = read_scalar(m->rest_rp + in.n_rows, st);
+    tr.mark("remainder counts + scan");
     alloc_rest(m, m->nnz_rest, st);
     if (sel.n_seg > 0 && (int64_t)sel.n_seg * bl > (int64_t)1 << 40)
         fail(HDCG_ERR_OUT_OF_MEMORY, "segments too large");
     m->seg = alloc_seg(sel.n_seg * bl, st);
+    tr.mark("allocate segments");
     const int64_t total = n_blocks * bl;
     if (total > 0) {
         fill_kernel<RP><<<grid_cap(ceil_div(total, 256)), 256, 0, st>>>(
@@ -712,6 +754,7 @@ static void finish_build(const CsrInput& in, int64_t bl, int64_t n_blocks, Selec
     }
     m->dia_slots = slots;
     m->max_seg_per_block = mx;
+    tr.mark("fill + slot count");
 }
 
 static void check_slab(const CsrInput& in, int64_t bl) {

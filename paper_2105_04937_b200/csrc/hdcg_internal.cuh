@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -231,11 +232,22 @@ cudaError_t cub_exclusive_sum_i64(void* tmp, size_t& bytes, const int64_t* in, i
                                   int64_t count, cudaStream_t st);
 
 // ---- small device helpers ----------------------------------------------------
+// Small arrays come from the stream-ordered pool; arrays of HDCG_BIG_ALLOC_MB (default
+// 16) or more from cudaMalloc: the pool maps fresh memory far more slowly than
+// cudaMalloc does (30 GB of config-4 segments: 174 ms against 1 ms; the whole
+// conversion 197 ms -> 36 ms, profiles/r03t_convert_alloc.log).  Either kind may be
+// released with cudaFreeAsync (dev_free) or cudaFree (matrix_release).
+inline size_t big_alloc_bytes() {
+    static const long long mb = getenv("HDCG_BIG_ALLOC_MB") ? atoll(getenv("HDCG_BIG_ALLOC_MB")) : 16;
+    return mb > 0 ? (size_t)mb << 20 : ~size_t(0);
+}
 template <class T>
 T* dev_alloc(int64_t count, cudaStream_t st) {
     if (count <= 0) return nullptr;
     void* p = nullptr;
-    HDCG_CUDA(cudaMallocAsync(&p, sizeof(T) * (size_t)count, st));
+    const size_t bytes = sizeof(T) * (size_t)count;
+    if (bytes >= big_alloc_bytes()) HDCG_CUDA(cudaMalloc(&p, bytes));
+    else HDCG_CUDA(cudaMallocAsync(&p, bytes, st));
     return static_cast<T*>(p);
 }
 template <class T>
