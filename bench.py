@@ -387,7 +387,7 @@ def run_ours(a):
     compute.spmv = timed_spmv
     launches0 = compute.launches
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local, period_s=0.005) as clocks:
+    with ClockSampler(local, period_s=0.001) as clocks:
         torch.cuda.synchronize()
         start.record()
         for _ in range(a.steps):
