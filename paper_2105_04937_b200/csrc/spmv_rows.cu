@@ -355,7 +355,9 @@ bool rest_rows_launch(const Matrix& m, const double* x_local, double* y, const d
     a.row0 = m.row0;
     a.r_lo = r0;
     a.r_hi = r1;
-    a.chunk_runs = ek && atoi(ek) > 0 ? atoi(ek) : 4 * W;
+    // two runs per warp and chunk: 95.7% / 96.2% of the HBM peak on configs 1 / 2 as CSR
+    // against 92.5% / 94.8% with four (profiles/r02s_ab_rows.log, chunk sweep)
+    a.chunk_runs = ek && atoi(ek) > 0 ? atoi(ek) : 2 * W;
     a.ns_log2 = 0;
     while ((1 << a.ns_log2) < NS) ++a.ns_log2;
     const size_t smem = (size_t)NS * CAP * 12 + sizeof(uint64_t) * 2 * NS;
