@@ -172,11 +172,15 @@ __device__ __forceinline__ bool hash_add(int32_t* keys, int32_t* cnts, int32_t o
     return false;
 }
 
+#ifndef HDCG_CENSUS_MINB
+#define HDCG_CENSUS_MINB 3
+#endif
 template <class RP>
-__global__ void __launch_bounds__(CENSUS_THREADS)
+__global__ void __launch_bounds__(CENSUS_THREADS, HDCG_CENSUS_MINB)
 census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t row0, int64_t bl,
                      int64_t n_blocks, double theta, int32_t* sel_count, int32_t* stash,
-                     int32_t* blk_status, int32_t* ovf_list, int32_t* ovf_count, int32_t* blk_rest) {
+                     int32_t* blk_status, int32_t* ovf_list, int32_t* ovf_count, int32_t* blk_rest,
+                     int bucket_filter) {
     __shared__ int32_t keys[HASH_CAP];
     __shared__ int32_t cnts[HASH_CAP];
     __shared__ int32_t sel[SEL_MAX];
@@ -220,6 +224,54 @@ census_select_kernel(RowPtr<RP> rp, const int32_t* col, int64_t n_rows, int64_t 
             }
         }
         __syncthreads();
+        // The table overflowed: more distinct offsets than slots (rows with scattered
+        // columns).  Only offsets with count >= theta * len matter, so count the
+        // entries per hash bucket first (no keys, no probing): an offset can pass the
+        // threshold only if its bucket's total does.  A second pass tallies exactly
+        // the offsets of those candidate buckets -- a handful of keys -- and the
+        // selection below proceeds as usual.  Exact: nothing that could be selected is
+        // left out.  (If every present offset qualifies -- theta * len <= 1 -- or the
+        // second pass overflows too, the block takes the sort path.)
+        if (s_overflow && bucket_filter && !((double)1 / (double)len >= theta)) {
+            __shared__ uint32_t cand[HASH_CAP / 32];
+            for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x) cnts[s] = 0;
+            for (int s = threadIdx.x; s < HASH_CAP / 32; s += blockDim.x) cand[s] = 0;
+            __syncthreads();
+            for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+                const int64_t gi = row0 + i, ke = rp[i + 1];
+                for (int64_t k = rp[i]; k < ke; ++k) {
+                    const int32_t off = (int32_t)((int64_t)col[k] - gi);
+                    const unsigned peers = __match_any_sync(__activemask(), off);
+                    if (lane == __ffs(peers) - 1)
+                        atomicAdd(&cnts[((uint32_t)off * 0x9E3779B1u) >> (32 - HASH_LOG2)], __popc(peers));
+                }
+            }
+            __syncthreads();
+            for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x)
+                if ((double)cnts[s] / (double)len >= theta) atomicOr(&cand[s >> 5], 1u << (s & 31));
+            __syncthreads();
+            for (int s = threadIdx.x; s < HASH_CAP; s += blockDim.x) {
+                keys[s] = EMPTY_KEY;
+                cnts[s] = 0;
+            }
+            if (threadIdx.x == 0) { s_overflow = 0; s_nused = 0; }
+            __syncthreads();
+            for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+                if (*vovf) break;
+                const int64_t gi = row0 + i, ke = rp[i + 1];
+                for (int64_t k = rp[i]; k < ke; ++k) {
+                    const int32_t off = (int32_t)((int64_t)col[k] - gi);
+                    const uint32_t h = ((uint32_t)off * 0x9E3779B1u) >> (32 - HASH_LOG2);
+                    if ((cand[h >> 5] >> (h & 31)) & 1u) {
+                        const unsigned peers = __match_any_sync(__activemask(), off);
+                        if (lane == __ffs(peers) - 1) {
+                            if (!hash_add(keys, cnts, off, __popc(peers), used, &s_nused)) *vovf = 1;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
         if (!s_overflow) {
             const int nu = s_nused;
             const int n_scan = nu <= USED_MAX ? nu : HASH_CAP;
@@ -602,9 +654,12 @@ static Selection select_blocked(const CsrInput& in, double theta, int64_t bl, in
     s.blk_rest = dev_alloc<int32_t>(n_blocks, st);
     // one thread per row for blocks narrower than the CTA
     const int threads = (int)std::min<int64_t>(CENSUS_THREADS, std::max<int64_t>(64, (bl + 31) / 32 * 32));
+    // HDCG_CENSUS_FILTER=0: overflowing blocks go straight to the sort path (A/B knob)
+    const char* ef = getenv("HDCG_CENSUS_FILTER");
+    const int bucket_filter = !ef || atoi(ef) != 0;
     census_select_kernel<RP><<<grid_cap(n_blocks), threads, 0, st>>>(
         rp, in.col, in.n_rows, in.row0, bl, n_blocks, theta, sel_count, stash, blk_status, ovf_list,
-        ovf_count, s.blk_rest);
+        ovf_count, s.blk_rest, bucket_filter);
     HDCG_LAUNCH_CHECK("census_select_kernel");
     int32_t flags[2] = {0, 0};
     HDCG_CUDA(cudaMemcpyAsync(flags, ovf_count, sizeof(flags), cudaMemcpyDeviceToHost, st));
