@@ -1060,3 +1060,38 @@ def test_concurrent_host_spmv_calls(port):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+def test_census_with_scattered_columns_every_threshold(port, monkeypatch):
+    """Blocks whose distinct offsets overflow the census hash table (rows with
+    scattered columns) go through the bucket filter -- count per hash bucket, then
+    an exact tally of the candidate buckets' offsets -- and, when that overflows
+    too (tiny theta) or every offset qualifies (theta * len <= 1), through the exact
+    sort path.  Formats bit-exact against the oracle for every threshold regime, with
+    partial diagonals of every fill level so that selections sit on both sides of
+    theta, with the filter on and off, for M-HDC and HDC."""
+    rng = np.random.default_rng(11)
+    n, bl = 20000, 4096
+    rows, cols = [], []
+    for off, fill in ((0, 1.0), (1, 0.9), (-3, 0.61), (7, 0.6), (-64, 0.59), (100, 0.3), (-1000, 0.05), (2048, 0.002)):
+        i = np.arange(max(0, -off), min(n, n - off))
+        i = i[rng.random(i.size) < fill]
+        rows.append(i)
+        cols.append(i + off)
+    r = np.repeat(np.arange(n), 12)  # 12 scattered columns per row
+    rows.append(r)
+    cols.append(rng.integers(0, n, r.size))
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    vals = rng.uniform(-1, 1, rows.size)
+    rp, col, val = synth.coo_to_csr(n, rows, cols, vals)
+    A = csr(rp, col, val)
+    x = synth.x_vector(n, 3)
+    for filt in ("1", "0"):
+        monkeypatch.setenv("HDCG_CENSUS_FILTER", filt)
+        for theta in (0.0, 1.0 / bl, 1.5 / bl, 0.001, 0.05, 0.3, 0.6, 0.9, 1.0):
+            m = H.to_mhdc(A, theta, bl)
+            ref = port.to_mhdc(rp, col, val, theta, bl)
+            assert_mhdc_equal(m, ref, (filt, theta))
+            assert H.spmv_mhdc(m, x).tobytes() == port.spmv_mhdc(ref, x).tobytes(), (filt, theta)
+    for theta in (0.0, 0.05, 0.6):
+        assert_mhdc_equal(H.to_hdc(A, theta), port.to_hdc(rp, col, val, theta), theta)
