@@ -81,3 +81,4 @@ def test_bench_two_ranks_on_one_gpu(tmp_path):
         assert two["result"]["y_checksum_lo_hi"] == one["result"]["y_checksum_lo_hi"]
         assert two["result"]["norm2_last_hex"] == one["result"]["norm2_last_hex"]
         assert two["config"]["nnz"] == one["config"]["nnz"]
+        assert two["e2e"]["result_checked"] is True  # the chunked host pipeline returned the slab's exact y
