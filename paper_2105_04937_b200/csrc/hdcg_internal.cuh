@@ -124,6 +124,12 @@ struct PipeCtx {
     double* dy = nullptr;
     cudaStream_t s[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
     std::vector<cudaEvent_t> events;
+    // pageable host vectors (what the reference's std::vector-based API hands over):
+    // pinned staging rings, allocated on the first such call (host_spmv.cu)
+    double* hx = nullptr;      // STAGE_SLOTS slots of slot_elems doubles each
+    double* hy = nullptr;
+    int64_t slot_elems = 0;
+    std::vector<cudaEvent_t> slot_ev;  // [0, S): x slot free again; [S, 2S): y slot filled
 };
 void pipe_ctx_release(PipeCtx* c);
 

@@ -12,8 +12,19 @@
 //   stream 2: chunk c's y rows are copied device->host as soon as its kernel ends.
 // With pinned host buffers H2D and D2H run concurrently (PCIe is full duplex),
 // so a call costs about max(8 n_cols, 8 n_rows) / PCIe bandwidth instead of the sum.
+//
+// Pageable vectors -- what the reference API hands over: std::vector storage behind
+// std::span (kernels.hpp:31-49) -- would make every cudaMemcpyAsync a synchronous,
+// single-threaded staged copy inside the driver (7 GB/s each way, no overlap: 19 ms
+// per call on config 1 against 3.4 ms pinned, slower than the reference on the
+// CPU).  For those the pipeline stages the pieces itself: a small pool of host
+// threads copies x piece p into a pinned ring slot while piece p-1 is on the wire,
+// and copies finished y chunks out of their pinned slots into the caller's vector.
 #include <algorithm>
+#include <condition_variable>
 #include <cstdlib>
+#include <cstring>
+#include <thread>
 
 #include "hdcg_internal.cuh"
 
@@ -111,6 +122,98 @@ PipeCtx* new_ctx(const Matrix* m) {
     return c;
 }
 
+// Blocking memcpy spread over a few host threads (the caller takes a share): one
+// core copies ~10 GB/s, a B200 host needs ~50 GB/s each way to keep PCIe busy.
+// Threads start on the first pageable call; HDCG_COPY_THREADS sets their number.
+class CopyPool {
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_work_, cv_done_;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+
+    static void slice(size_t n, int part, int parts, size_t* a, size_t* b) {
+        *a = (n * (size_t)part / (size_t)parts) & ~size_t(63);
+        *b = part + 1 == parts ? n : (n * (size_t)(part + 1) / (size_t)parts) & ~size_t(63);
+    }
+    void run(int id) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_work_.wait(lk, [&] { return stop_ || gen_ != seen; });
+            if (stop_) return;
+            seen = gen_;
+            char* d = dst_;
+            const char* s = src_;
+            const size_t n = bytes_;
+            lk.unlock();
+            size_t a, b;
+            slice(n, id + 1, (int)workers_.size() + 1, &a, &b);
+            if (b > a) std::memcpy(d + a, s + a, b - a);
+            lk.lock();
+            if (--pending_ == 0) cv_done_.notify_one();
+        }
+    }
+
+public:
+    CopyPool() {
+        const char* e = getenv("HDCG_COPY_THREADS");
+        const int hc = (int)std::thread::hardware_concurrency();
+        int n = e ? atoi(e) : std::min(12, std::max(2, hc - 2));
+        n = std::max(1, n) - 1;  // + the calling thread
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(i); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_work_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    void copy(void* dst, const void* src, size_t n) {
+        if (n < (size_t)1 << 20 || workers_.empty()) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        std::lock_guard<std::mutex> call(call_mu_);  // one spread copy at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            dst_ = (char*)dst;
+            src_ = (const char*)src;
+            bytes_ = n;
+            pending_ = (int)workers_.size();
+            ++gen_;
+        }
+        cv_work_.notify_all();
+        size_t a, b;
+        slice(n, 0, (int)workers_.size() + 1, &a, &b);
+        if (b > a) std::memcpy((char*)dst + a, (const char*)src + a, b - a);
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_done_.wait(lk, [&] { return pending_ == 0; });
+    }
+};
+
+constexpr int STAGE_SLOTS = 4;
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes at;
+    const cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();  // older drivers report unregistered host memory as an error
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
+}
+
 // Borrow an idle pipeline context of m (creating one when every context is busy);
 // returned to the pool when the call ends, also on error.
 struct Borrow {
@@ -139,6 +242,10 @@ void pipe_ctx_release(PipeCtx* c) {
     if (!c) return;
     cudaFree(c->dx);
     cudaFree(c->dy);
+    cudaFreeHost(c->hx);
+    cudaFreeHost(c->hy);
+    for (cudaEvent_t e : c->slot_ev)
+        if (e) cudaEventDestroy(e);
     for (cudaStream_t s : c->s)
         if (s) cudaStreamDestroy(s);
     for (cudaEvent_t e : c->events)
@@ -155,34 +262,98 @@ void spmv_host_pipelined(Matrix* m, const double* x, double* y) {
     const int64_t nc = (int64_t)m->chunk_blocks.size() - 1;
     cudaEvent_t* ev_in = ctx->events.data();
     cudaEvent_t* ev_k = ctx->events.data() + np;
+    const Tiling t = tiling_of(*m);
+    auto chunk_rows = [&](int64_t c, int64_t* r0, int64_t* r1) {
+        const int64_t q0 = m->chunk_blocks[c], q1 = m->chunk_blocks[c + 1];
+        int64_t dummy;
+        tile_rows(q0, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, r0, &dummy);
+        tile_rows(q1 - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &dummy, r1);
+        *r0 = std::min(*r0, m->n_rows);
+    };
+    static const bool stage_off = getenv("HDCG_STAGE_PAGEABLE") && atoi(getenv("HDCG_STAGE_PAGEABLE")) == 0;
+    const bool stage_x = !stage_off && is_pageable(x), stage_y = !stage_off && is_pageable(y);
+    if (stage_x || stage_y) {
+        if (!ctx->hx) {  // pinned rings, sized for the largest x piece / y chunk of this matrix
+            int64_t mx = 1;
+            for (int64_t p = 0; p < np; ++p) mx = std::max(mx, m->x_pieces[p + 1] - m->x_pieces[p]);
+            for (int64_t c = 0; c < nc; ++c) {
+                int64_t r0, r1;
+                chunk_rows(c, &r0, &r1);
+                mx = std::max(mx, r1 - r0);
+            }
+            ctx->slot_elems = mx;
+            HDCG_CUDA(cudaHostAlloc(&ctx->hx, sizeof(double) * mx * STAGE_SLOTS, cudaHostAllocDefault));
+            HDCG_CUDA(cudaHostAlloc(&ctx->hy, sizeof(double) * mx * STAGE_SLOTS, cudaHostAllocDefault));
+            ctx->slot_ev.assign(2 * STAGE_SLOTS, nullptr);
+            for (auto& e : ctx->slot_ev) HDCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
+    CopyPool* pool = (stage_x || stage_y) ? &CopyPool::get() : nullptr;
+    cudaEvent_t* ev_xfree = ctx->slot_ev.data();
+    cudaEvent_t* ev_yfull = ctx->slot_ev.data() + STAGE_SLOTS;
+
+    int64_t c_next = 0;     // next chunk to launch
+    int64_t c_drained = 0;  // staged y chunks [0, c_drained) are in the caller's vector
+    int64_t p_done = -1;
+    auto drain = [&](int64_t c) {  // y chunk c: pinned slot -> caller's vector
+        int64_t r0, r1;
+        chunk_rows(c, &r0, &r1);
+        HDCG_CUDA(cudaEventSynchronize(ev_yfull[c % STAGE_SLOTS]));
+        if (r1 > r0) pool->copy(y + r0, ctx->hy + (c % STAGE_SLOTS) * ctx->slot_elems, sizeof(double) * (r1 - r0));
+    };
+    auto launch_ready = [&](int64_t pieces_sent) {
+        // every chunk whose x is on its way (pieces [0, pieces_sent) are enqueued)
+        const int64_t have = m->x_pieces[pieces_sent];
+        while (c_next < nc && (m->chunk_x_hi[c_next] <= have || pieces_sent == np)) {
+            const int64_t c = c_next++;
+            const int64_t need = m->chunk_x_hi[c];
+            int64_t p = p_done;
+            while (p + 1 < np && m->x_pieces[p + 1] < need) ++p;
+            if (need > 0 && p < 0) p = 0;
+            if (p > p_done) {
+                HDCG_CUDA(cudaStreamWaitEvent(s_k, ev_in[p], 0));
+                p_done = p;
+            }
+            spmv_launch_tiles(*m, ctx->dx + m->row0, ctx->dy, m->chunk_blocks[c], m->chunk_blocks[c + 1], nullptr,
+                              nullptr, s_k);
+            HDCG_CUDA(cudaEventRecord(ev_k[c], s_k));
+            HDCG_CUDA(cudaStreamWaitEvent(s_out, ev_k[c], 0));
+            int64_t r0, r1;
+            chunk_rows(c, &r0, &r1);
+            if (stage_y) {
+                if (c >= STAGE_SLOTS) {  // the slot's previous chunk must be out first
+                    for (; c_drained <= c - STAGE_SLOTS; ++c_drained) drain(c_drained);
+                }
+                if (r1 > r0)
+                    HDCG_CUDA(cudaMemcpyAsync(ctx->hy + (c % STAGE_SLOTS) * ctx->slot_elems, ctx->dy + r0,
+                                              sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost, s_out));
+                HDCG_CUDA(cudaEventRecord(ev_yfull[c % STAGE_SLOTS], s_out));
+            } else if (r1 > r0) {
+                HDCG_CUDA(cudaMemcpyAsync(y + r0, ctx->dy + r0, sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost,
+                                          s_out));
+            }
+        }
+    };
     for (int64_t p = 0; p < np; ++p) {
         const int64_t a = m->x_pieces[p], e = m->x_pieces[p + 1];
-        if (e > a) HDCG_CUDA(cudaMemcpyAsync(ctx->dx + a, x + a, sizeof(double) * (e - a), cudaMemcpyHostToDevice, s_in));
-        HDCG_CUDA(cudaEventRecord(ev_in[p], s_in));
-    }
-    const Tiling t = tiling_of(*m);
-    int64_t p_done = -1;
-    for (int64_t c = 0; c < nc; ++c) {
-        // wait for the x pieces up to the one holding column chunk_x_hi[c]-1
-        const int64_t need = m->chunk_x_hi[c];
-        int64_t p = p_done;
-        while (p + 1 < np && m->x_pieces[p + 1] < need) ++p;
-        if (need > 0 && p < 0) p = 0;
-        if (p > p_done) {
-            HDCG_CUDA(cudaStreamWaitEvent(s_k, ev_in[p], 0));
-            p_done = p;
+        if (e > a) {
+            if (stage_x) {
+                double* slot = ctx->hx + (p % STAGE_SLOTS) * ctx->slot_elems;
+                if (p >= STAGE_SLOTS) HDCG_CUDA(cudaEventSynchronize(ev_xfree[p % STAGE_SLOTS]));
+                pool->copy(slot, x + a, sizeof(double) * (e - a));
+                HDCG_CUDA(cudaMemcpyAsync(ctx->dx + a, slot, sizeof(double) * (e - a), cudaMemcpyHostToDevice, s_in));
+                HDCG_CUDA(cudaEventRecord(ev_xfree[p % STAGE_SLOTS], s_in));
+            } else {
+                HDCG_CUDA(cudaMemcpyAsync(ctx->dx + a, x + a, sizeof(double) * (e - a), cudaMemcpyHostToDevice, s_in));
+            }
         }
-        const int64_t q0 = m->chunk_blocks[c], q1 = m->chunk_blocks[c + 1];
-        spmv_launch_tiles(*m, ctx->dx + m->row0, ctx->dy, q0, q1, nullptr, nullptr, s_k);
-        HDCG_CUDA(cudaEventRecord(ev_k[c], s_k));
-        HDCG_CUDA(cudaStreamWaitEvent(s_out, ev_k[c], 0));
-        int64_t r0, r1, dummy;
-        tile_rows(q0, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &r0, &dummy);
-        tile_rows(q1 - 1, t.tiles_per_block, t.blocks_per_tile, t.tile_rows, m->bl, m->n_rows, &dummy, &r1);
-        r0 = std::min(r0, m->n_rows);
-        if (r1 > r0)
-            HDCG_CUDA(cudaMemcpyAsync(y + r0, ctx->dy + r0, sizeof(double) * (r1 - r0), cudaMemcpyDeviceToHost, s_out));
+        HDCG_CUDA(cudaEventRecord(ev_in[p], s_in));
+        // staging is host work: launch what can already run, so kernels and y copies overlap it
+        if (stage_x || stage_y) launch_ready(p + 1);
     }
+    launch_ready(np);
+    if (stage_y)
+        for (; c_drained < nc; ++c_drained) drain(c_drained);
     HDCG_CUDA(cudaStreamSynchronize(s_out));
     HDCG_CUDA(cudaStreamSynchronize(s_in));
 }
