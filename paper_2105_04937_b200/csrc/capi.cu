@@ -79,7 +79,7 @@ struct Staged {
         if (on_device || count <= 0 || p == nullptr) return p;
         T* d = dev_alloc<T>(count, st);
         owned.push_back(d);
-        HDCG_CUDA(cudaMemcpyAsync(d, p, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+        copy_h2d(d, p, sizeof(T) * count, st);
         return d;
     }
 };
@@ -113,13 +113,13 @@ void account(Matrix* m) {
 template <class T>
 T* upload(const T* host, int64_t count, cudaStream_t st) {
     T* d = dev_alloc<T>(count, st);
-    if (count > 0) HDCG_CUDA(cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+    if (count > 0) copy_h2d(d, host, sizeof(T) * count, st);
     return d;
 }
 
 double* upload_seg(const double* host, int64_t count, cudaStream_t st) {
     double* d = alloc_seg(count, st);
-    if (count > 0) HDCG_CUDA(cudaMemcpyAsync(d, host, sizeof(double) * count, cudaMemcpyHostToDevice, st));
+    if (count > 0) copy_h2d(d, host, sizeof(double) * count, st);
     return d;
 }
 
@@ -373,10 +373,8 @@ hdcg_status hdcg_upload_mhdc(int64_t n, int64_t bl, const int32_t* dia_ptr, int6
             m->rest_rp = upload(rest_row_ptr, n + 1, st);
             alloc_rest(m, nnz_rest, st);
             if (nnz_rest > 0) {
-                HDCG_CUDA(cudaMemcpyAsync(m->rest_col, rest_col_ind, sizeof(int32_t) * nnz_rest,
-                                          cudaMemcpyHostToDevice, st));
-                HDCG_CUDA(cudaMemcpyAsync(m->rest_val, rest_values, sizeof(double) * nnz_rest,
-                                          cudaMemcpyHostToDevice, st));
+                copy_h2d(m->rest_col, rest_col_ind, sizeof(int32_t) * nnz_rest, st);
+                copy_h2d(m->rest_val, rest_values, sizeof(double) * nnz_rest, st);
             }
             int64_t slots = 0, dia_nnz = 0;
             for (int64_t b = 0; b < m->n_blocks; ++b) {
@@ -438,10 +436,8 @@ hdcg_status hdcg_upload_hdc(int64_t n, int64_t n_diag, const int32_t* offsets, c
             m->rest_rp = upload(rest_row_ptr, n + 1, st);
             alloc_rest(m, nnz_rest, st);
             if (nnz_rest > 0) {
-                HDCG_CUDA(cudaMemcpyAsync(m->rest_col, rest_col_ind, sizeof(int32_t) * nnz_rest,
-                                          cudaMemcpyHostToDevice, st));
-                HDCG_CUDA(cudaMemcpyAsync(m->rest_val, rest_values, sizeof(double) * nnz_rest,
-                                          cudaMemcpyHostToDevice, st));
+                copy_h2d(m->rest_col, rest_col_ind, sizeof(int32_t) * nnz_rest, st);
+                copy_h2d(m->rest_val, rest_values, sizeof(double) * nnz_rest, st);
             }
             int64_t dia_nnz = 0;
             for (int64_t k = 0; k < m->n_seg * m->bl; ++k) dia_nnz += lanes[k] != 0.0;
@@ -511,7 +507,10 @@ hdcg_status hdcg_export(hdcg_matrix h, int32_t* dia_ptr, int32_t* dia_offsets, d
         const Matrix* m = unwrap(h);
         const DeviceGuard dg(m->device);
         auto cp = [](void* dst, const void* src, size_t bytes) {
-            if (dst && src && bytes) HDCG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+            if (dst && src && bytes) {
+                copy_d2h(dst, src, bytes, nullptr);  // staged through pinned memory when dst is pageable
+                HDCG_CUDA(cudaStreamSynchronize(nullptr));
+            }
         };
         cp(dia_ptr, m->dia_ptr, sizeof(int32_t) * (m->n_blocks + 1));
         if (dia_ptr && m->n_blocks == 0) dia_ptr[0] = 0;
@@ -547,7 +546,10 @@ hdcg_status hdcg_export_blocks(hdcg_matrix h, int64_t block_begin, int64_t block
             counts[1] = e[1] - e[0];
         }
         auto cp = [](void* dst, const void* src, size_t bytes) {
-            if (dst && src && bytes) HDCG_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+            if (dst && src && bytes) {
+                copy_d2h(dst, src, bytes, nullptr);  // staged through pinned memory when dst is pageable
+                HDCG_CUDA(cudaStreamSynchronize(nullptr));
+            }
         };
         if (dia_ptr) {
             if (m->n_blocks > 0) cp(dia_ptr, m->dia_ptr + block_begin, sizeof(int32_t) * (nb + 1));

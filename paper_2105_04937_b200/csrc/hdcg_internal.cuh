@@ -211,6 +211,11 @@ void membench(int64_t n, int mode, int n_loops, int n_ites, double* best_s, doub
 // synchronous SpMV on host buffers, H2D / kernel / D2H overlapped chunk by chunk
 void spmv_host_pipelined(Matrix* m, const double* x_host, double* y_host);
 void tree_sum_launch(const double* vals, int64_t count, double* out, cudaStream_t st);
+// bulk host <-> device copies, fast for pageable host memory too (host_spmv.cu): large
+// pageable transfers are staged through a pinned ring and have completed on return;
+// anything else is a cudaMemcpyAsync on st
+void copy_h2d(void* dev, const void* host, size_t bytes, cudaStream_t st);
+void copy_d2h(void* host, const void* dev, size_t bytes, cudaStream_t st);
 
 // ---- converters (convert.cu) ------------------------------------------------
 struct CsrInput {

@@ -238,6 +238,83 @@ struct Borrow {
 
 }  // namespace
 
+// ---- bulk host <-> device copies for the upload / export entry points -------------
+// The reference's containers are std::vectors (pageable): a plain cudaMemcpy of them
+// runs at ~7 GB/s through the driver's own staging.  Large pageable transfers go
+// through a process-wide pinned ring instead, filled / drained by the copy pool while
+// the previous slot is on the wire.  Pinned or registered host memory, and small
+// transfers, take cudaMemcpyAsync directly.
+namespace {
+constexpr size_t BULK_SLOT = (size_t)16 << 20;
+constexpr int BULK_SLOTS = 4;
+struct BulkRing {
+    std::mutex mu;  // one staged transfer at a time
+    char* ring = nullptr;
+    cudaEvent_t ev[BULK_SLOTS] = {};
+    void ensure() {
+        if (ring) return;
+        HDCG_CUDA(cudaHostAlloc(&ring, BULK_SLOT * BULK_SLOTS, cudaHostAllocPortable));
+        for (auto& e : ev) HDCG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+};
+BulkRing& bulk_ring() {
+    static BulkRing r;  // lives until process exit (pinned memory is released with the context)
+    return r;
+}
+bool stage_bulk(const void* host, size_t bytes) {
+    static const bool off = getenv("HDCG_STAGE_PAGEABLE") && atoi(getenv("HDCG_STAGE_PAGEABLE")) == 0;
+    return !off && bytes >= ((size_t)8 << 20) && is_pageable(host);
+}
+}  // namespace
+
+void copy_h2d(void* dev, const void* host, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (!stage_bulk(host, bytes)) {
+        HDCG_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    BulkRing& r = bulk_ring();
+    std::lock_guard<std::mutex> lock(r.mu);
+    r.ensure();
+    CopyPool& pool = CopyPool::get();
+    int i = 0;
+    for (size_t off = 0; off < bytes; off += BULK_SLOT, ++i) {
+        const size_t n = std::min(BULK_SLOT, bytes - off);
+        const int s = i % BULK_SLOTS;
+        if (i >= BULK_SLOTS) HDCG_CUDA(cudaEventSynchronize(r.ev[s]));
+        pool.copy(r.ring + s * BULK_SLOT, (const char*)host + off, n);
+        HDCG_CUDA(cudaMemcpyAsync((char*)dev + off, r.ring + s * BULK_SLOT, n, cudaMemcpyHostToDevice, st));
+        HDCG_CUDA(cudaEventRecord(r.ev[s], st));
+    }
+    HDCG_CUDA(cudaStreamSynchronize(st));  // the ring is free again when this returns
+}
+
+void copy_d2h(void* host, const void* dev, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (!stage_bulk(host, bytes)) {
+        HDCG_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st));
+        return;
+    }
+    BulkRing& r = bulk_ring();
+    std::lock_guard<std::mutex> lock(r.mu);
+    r.ensure();
+    CopyPool& pool = CopyPool::get();
+    const int total = (int)((bytes + BULK_SLOT - 1) / BULK_SLOT);
+    auto finish = [&](int j) {  // slot of piece j -> the caller's memory
+        const size_t off = (size_t)j * BULK_SLOT, n = std::min(BULK_SLOT, bytes - off);
+        HDCG_CUDA(cudaEventSynchronize(r.ev[j % BULK_SLOTS]));
+        pool.copy((char*)host + off, r.ring + (j % BULK_SLOTS) * BULK_SLOT, n);
+    };
+    for (int i = 0; i < total; ++i) {
+        const size_t off = (size_t)i * BULK_SLOT, n = std::min(BULK_SLOT, bytes - off);
+        if (i >= BULK_SLOTS) finish(i - BULK_SLOTS);
+        HDCG_CUDA(cudaMemcpyAsync(r.ring + (i % BULK_SLOTS) * BULK_SLOT, (const char*)dev + off, n,
+                                  cudaMemcpyDeviceToHost, st));
+        HDCG_CUDA(cudaEventRecord(r.ev[i % BULK_SLOTS], st));
+    }
+    for (int j = std::max(0, total - BULK_SLOTS); j < total; ++j) finish(j);
+}
+
 void pipe_ctx_release(PipeCtx* c) {
     if (!c) return;
     cudaFree(c->dx);
