@@ -97,6 +97,19 @@ std::vector<index_t> widen(const std::vector<T>& v) {
     return std::vector<index_t>(v.begin(), v.end());
 }
 
+// ---- optional lifetime tracking (hdc_gpu_shim_lifetime.cpp) ---------------------
+// When that file is linked too, operator delete reports released arrays and a
+// cached matrix whose arrays are all still alive is used without re-hashing them.
+}  // namespace
+extern "C" {
+int hdcg_shim_lifetime_tracking() __attribute__((weak));
+int hdcg_shim_track(const void* p) __attribute__((weak));
+int hdcg_shim_alive(int slot) __attribute__((weak));
+void hdcg_shim_untrack(int slot) __attribute__((weak));
+}
+namespace {
+inline bool lifetime_mode() { return hdcg_shim_lifetime_tracking != nullptr && hdcg_shim_lifetime_tracking() == 1; }
+
 // ---- device cache -------------------------------------------------------------
 // A host matrix is identified by its array addresses and sizes AND a hash of
 // every byte of its arrays.  The hash is recomputed on every lookup, so a matrix
@@ -187,12 +200,39 @@ struct Entry {
     uint64_t hash;
     hdcg_matrix h;
     int64_t bytes;
+    int slots[3] = {-2, -2, -2};  // lifetime-tracker slots of key.a/b/c (-2: not tracked, -1: table full)
 };
+
+inline void untrack(Entry& e) {
+    if (!lifetime_mode()) return;
+    for (int& s : e.slots) {
+        if (s >= 0) hdcg_shim_untrack(s);
+        s = -2;
+    }
+}
 
 class Cache {
 public:
     ~Cache() {
-        for (auto& e : lru_) hdcg_free(e.h);
+        for (auto& e : lru_) {
+            untrack(e);
+            hdcg_free(e.h);
+        }
+    }
+    // Lifetime mode only: the device copy at key k when none of the matrix's arrays
+    // has been released since it was cached -- no hash, the arrays are not read.
+    hdcg_matrix find_live(const Key& k) {
+        if (!lifetime_mode()) return nullptr;
+        std::lock_guard<std::mutex> lock(mu_);
+        for (auto it = lru_.begin(); it != lru_.end(); ++it)
+            if (it->key == k) {
+                const void* ptrs[3] = {k.a, k.b, k.c};
+                for (int j = 0; j < 3; ++j)
+                    if (ptrs[j] != nullptr && !(it->slots[j] >= 0 && hdcg_shim_alive(it->slots[j]))) return nullptr;
+                lru_.splice(lru_.begin(), lru_, it);
+                return it->h;
+            }
+        return nullptr;
     }
     // the device copy of (key, hash); an entry at the same key with a different
     // hash (storage reused or contents changed) is freed
@@ -205,6 +245,7 @@ public:
                     return it->h;
                 }
                 bytes_ -= it->bytes;
+                untrack(*it);
                 hdcg_free(it->h);
                 lru_.erase(it);
                 return nullptr;
@@ -218,15 +259,21 @@ public:
         for (auto it = lru_.begin(); it != lru_.end(); ++it)
             if (it->key == k) {  // superseded
                 bytes_ -= it->bytes;
+                untrack(*it);
                 hdcg_free(it->h);
                 lru_.erase(it);
                 break;
             }
         lru_.push_front(Entry{k, hash, h, info.device_bytes});
+        if (lifetime_mode()) {
+            const void* ptrs[3] = {k.a, k.b, k.c};
+            for (int j = 0; j < 3; ++j) lru_.front().slots[j] = ptrs[j] ? hdcg_shim_track(ptrs[j]) : -2;
+        }
         bytes_ += info.device_bytes;
         // the newest entry always stays (its caller is about to use it)
         while (lru_.size() > 1 && (lru_.size() > kMaxEntries || bytes_ > kMaxBytes)) {
             bytes_ -= lru_.back().bytes;
+            untrack(lru_.back());
             hdcg_free(lru_.back().h);
             lru_.pop_back();
         }
@@ -256,6 +303,24 @@ struct Ident {
     uint64_t hash;
 };
 
+// the address / size part of a matrix's identity (no array is read)
+Key key_of(const CsrMatrix& m) {
+    return Key{K_CSR, m.values().data(), m.col_ind().data(), m.row_ptr().data(), m.values().size(),
+               m.col_ind().size(), m.row_ptr().size()};
+}
+Key key_of(const DiaMatrix& m) {
+    return Key{K_DIA, m.lanes().data(), m.offsets().data(), nullptr, m.lanes().size(), m.offsets().size(), 0};
+}
+Key key_of(const HdcMatrix& m) {
+    const Key d = key_of(m.dia()), c = key_of(m.csr());
+    return Key{K_HDC, d.a, d.b, c.a, d.na, d.nb, c.na};
+}
+Key key_of(const MHdcMatrix& m) {
+    const Key c = key_of(m.csr());
+    return Key{K_MHDC, m.segments().data(), m.dia_offsets().data(), c.a, m.segments().size(),
+               m.dia_offsets().size(), c.na};
+}
+
 Ident ident(const CsrMatrix& m) {
     const uint64_t h = content_hash(m.values(), content_hash(m.col_ind(), content_hash(m.row_ptr(), m.n())));
     return {Key{K_CSR, m.values().data(), m.col_ind().data(), m.row_ptr().data(), m.values().size(),
@@ -279,6 +344,7 @@ Ident ident(const MHdcMatrix& m) {
 }
 
 hdcg_matrix device_of(const CsrMatrix& m) {
+    if (hdcg_matrix live = cache().find_live(key_of(m))) return live;  // lifetime mode: no hashing
     const Ident id = ident(m);
     if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     const RowPtrArg rp(m.row_ptr());
@@ -307,6 +373,7 @@ hdcg_matrix upload_hdc(index_t n, std::span<const index_t> offsets, std::span<co
 }
 
 hdcg_matrix device_of(const DiaMatrix& m) {
+    if (hdcg_matrix live = cache().find_live(key_of(m))) return live;  // lifetime mode: no hashing
     const Ident id = ident(m);
     if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     hdcg_matrix h = upload_hdc(m.n(), m.offsets(), m.lanes(), nullptr);
@@ -315,6 +382,7 @@ hdcg_matrix device_of(const DiaMatrix& m) {
 }
 
 hdcg_matrix device_of(const HdcMatrix& m) {
+    if (hdcg_matrix live = cache().find_live(key_of(m))) return live;  // lifetime mode: no hashing
     const Ident id = ident(m);
     if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     hdcg_matrix h = upload_hdc(m.n(), m.dia().offsets(), m.dia().lanes(), &m.csr());
@@ -323,6 +391,7 @@ hdcg_matrix device_of(const HdcMatrix& m) {
 }
 
 hdcg_matrix device_of(const MHdcMatrix& m) {
+    if (hdcg_matrix live = cache().find_live(key_of(m))) return live;  // lifetime mode: no hashing
     const Ident id = ident(m);
     if (hdcg_matrix h = cache().find(id.key, id.hash)) return h;
     const I32View dp(m.dia_ptr()), offs(m.dia_offsets()), rp(m.csr().row_ptr()), col(m.csr().col_ind());

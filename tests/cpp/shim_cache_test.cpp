@@ -12,6 +12,9 @@
 //      constructed (storage usually reused by the allocator);
 //   3. the same for a CSR through spmv_csr.
 // Exit code 0 = all pass; prints the failing case otherwise.
+// -DSHIM_LIFETIME (linked with hdc_gpu_shim_lifetime.cpp): the in-place cases are
+// skipped -- that build trusts the reference's immutability and tracks
+// the release of the host storage instead of re-hashing it on every call.
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -93,6 +96,9 @@ int main() {
     for (index_t i = 0; i < n; ++i) x[i] = 1.0 / (1.0 + (i % 1013));
 
     // 1. in-place change of one segment value (same addresses, same sizes)
+    // (not in the lifetime-tracking build: it trusts the reference's immutability,
+    // SPEC.md:94, and only drops a device copy when the host storage is released)
+#ifndef SHIM_LIFETIME
     {
         MHdcMatrix a = to_mhdc(make_csr(n, 0.0), 0.6, bl);
         std::vector<real_t> y(n);
@@ -116,6 +122,7 @@ int main() {
             expect(same(y, host_mhdc(a, x)), "remainder value changed in place");
         }
     }
+#endif
     // 2. destroy / re-create a same-shape matrix with one value different
     {
         const void* prev_seg = nullptr;
@@ -149,10 +156,12 @@ int main() {
         std::vector<real_t> y(n);
         spmv_csr(c, x, y);
         expect(same(y, host_csr(c, x)), "spmv_csr first call");
+#ifndef SHIM_LIFETIME  // in-place changes are outside the lifetime-tracking build's contract
         real_t* q = const_cast<real_t*>(c.values().data()) + c.values().size() / 2 + 77;
         *q *= 3.0;
         spmv_csr(c, x, y);
         expect(same(y, host_csr(c, x)), "spmv_csr after in-place change");
+#endif
         for (int round = 1; round < 3; ++round) {
             CsrMatrix d = make_csr(n, 0.5 * round);
             spmv_csr(d, x, y);

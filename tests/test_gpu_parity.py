@@ -703,6 +703,24 @@ def test_shim_cache_never_serves_stale_matrices():
     assert "all passed" in r.stdout
 
 
+LIFETIME_BINS = [os.path.join(os.path.dirname(ACCEPT), b) for b in ("acceptance_gpu_lifetime", "shim_cache_test_lifetime")]
+
+
+@pytest.mark.skipif(not all(os.path.exists(b) for b in LIFETIME_BINS), reason="lifetime builds missing (need /root/reference)")
+def test_shim_with_lifetime_tracking():
+    """The shim linked with its optional companion hdc_gpu_shim_lifetime.cpp (operator
+    delete reports released arrays, so a cached matrix whose storage is still alive is
+    used without re-hashing it): the reference's acceptance program passes all 8
+    criteria, and matrices destroyed and re-created at reused addresses never get a
+    stale device copy (the in-place cases are outside that build's contract)."""
+    r = subprocess.run([LIFETIME_BINS[0]], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(ACCEPT))
+    assert r.returncode == 0 and "all 8 criteria passed" in r.stdout, r.stdout + r.stderr
+    r = subprocess.run([LIFETIME_BINS[1]], capture_output=True, text=True, timeout=600, cwd=os.path.dirname(ACCEPT))
+    print(r.stdout)
+    assert r.returncode == 0 and "all passed" in r.stdout, r.stdout + r.stderr
+    assert "storage reused" in r.stdout  # the hazard actually occurred in this run
+
+
 @pytest.mark.parametrize("rest_mode", [H.REST_DEFAULT, H.REST_GLOBAL, H.REST_SPLIT, H.REST_FUSED])
 def test_remainder_paths(port, rest_mode):
     """The TMA kernel's ways of summing the CSR remainder (consumers load it from
