@@ -241,6 +241,14 @@ public:
         for (auto it = lru_.begin(); it != lru_.end(); ++it)
             if (it->key == k) {
                 if (it->hash == hash) {
+                    if (lifetime_mode()) {  // same contents at re-used storage: track the new arrays
+                        const void* ptrs[3] = {k.a, k.b, k.c};
+                        for (int j = 0; j < 3; ++j)
+                            if (ptrs[j] != nullptr && !(it->slots[j] >= 0 && hdcg_shim_alive(it->slots[j]))) {
+                                if (it->slots[j] >= 0) hdcg_shim_untrack(it->slots[j]);
+                                it->slots[j] = hdcg_shim_track(ptrs[j]);
+                            }
+                    }
                     lru_.splice(lru_.begin(), lru_, it);
                     return it->h;
                 }
