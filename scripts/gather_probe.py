@@ -13,7 +13,12 @@ import sys
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-L = ctypes.CDLL(os.path.join(HERE, "libgather_probe.so"))
+_SO = os.path.join(HERE, "libgather_probe.so")
+if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(os.path.join(HERE, "gather_probe.cu")):
+    import subprocess
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-shared", "-Xcompiler",
+                    "-fPIC", "-o", _SO, os.path.join(HERE, "gather_probe.cu")], check=True)
+L = ctypes.CDLL(_SO)
 P = ctypes.c_void_p
 L.gp_probe.argtypes = [P, P, P, P, P] + [ctypes.c_int] * 8 + [P]
 L.gp_pure.argtypes = [P, P] + [ctypes.c_int] * 6 + [P]
